@@ -1,0 +1,233 @@
+/*
+ * btnn_cuda.h — C ABI of libbtnn_cuda.so, the B200 (sm_100a) implementation of the
+ * btnn binarized-network hot path (arXiv 2006.16578, BTC-BNN).
+ *
+ * The reference (`/root/reference/proj/include/btnn`) is a header-only C++20 library
+ * with no FFI; its public surface is the C++ layer/model API. Every entry point below
+ * replaces exactly one of those functions, takes plain pointers and sizes in the
+ * reference's own bit layouts (LSB-first uint64 words, plain/fsb, HWNC/KKOC/PQNO), and
+ * returns a status code that mirrors the reference's exception taxonomy
+ * (common.hpp:14-32). Host buffers in, host buffers out, synchronous — like the
+ * reference calls. The C++ drop-in adapter `include/btnn/cuda.hpp` marshals the
+ * reference value types onto these calls and re-throws the same exception types.
+ *
+ * Each function cites the reference interface it replaces (file:line, relative to
+ * proj/include/btnn/).
+ */
+#ifndef BTNN_CUDA_H_
+#define BTNN_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BTNN_CUDA_ABI_VERSION 1
+
+/* Status codes: 0 ok; 1..4 = the reference's four exception types (common.hpp:14-32). */
+enum {
+  BTNN_OK = 0,
+  BTNN_INVALID_INPUT = 1,     /* btnn::invalid_input      (common.hpp:14) */
+  BTNN_UNSUPPORTED_SHAPE = 2, /* btnn::unsupported_shape  (common.hpp:19) */
+  BTNN_IO_ERROR = 3,          /* btnn::io_error           (common.hpp:24) */
+  BTNN_VALIDATION_ERROR = 4,  /* btnn::validation_error   (common.hpp:29) */
+  BTNN_CUDA_ERROR = 5         /* device / driver failure (no reference analog) */
+};
+
+/* Matrix layouts (bit_matrix.hpp:21). */
+enum { BTNN_ROW_PACKED = 0, BTNN_COL_PACKED = 1, BTNN_FSB_ROW = 2, BTNN_FSB_COL = 3 };
+/* BMM variants (bmm.hpp:40). On the GPU the variant only selects operand validation. */
+enum { BTNN_BMM_NAIVE = 0, BTNN_BMM_BLOCKED = 1, BTNN_BMM_FSB = 2 };
+/* Threshold kinds (layer_math.hpp:38). */
+enum { BTNN_GEQ = 0, BTNN_LEQ = 1, BTNN_CONST_PLUS = 2, BTNN_CONST_MINUS = 3 };
+/* Layer kinds (model.hpp:17-23). */
+enum { BTNN_FIRST_CONV_BWN = 0, BTNN_BIT_CONV = 1, BTNN_OR_POOL = 2, BTNN_BIT_FC = 3, BTNN_LAST_FC = 4 };
+
+/* BitMatrix shape (bit_matrix.hpp:61-132). bh/bw: FsbGeometry (:36), ignored for packed layouts. */
+typedef struct {
+  size_t rows, cols;
+  int layout;
+  size_t bh, bw;
+} btnn_matrix_desc;
+
+/* BmmOptions (bmm.hpp:49-53) incl. BmmBlocking (:43-47). threads is accepted and ignored. */
+typedef struct {
+  int variant;
+  size_t blk_rows, blk_cols, blk_k_bits;
+  int threads;
+} btnn_bmm_options;
+
+/* BitTensorHWNC shape (tensors.hpp:71-114). */
+typedef struct {
+  size_t height, width, batch, channels;
+  int tiled;
+  size_t bh, bw;
+} btnn_act_desc;
+
+/* BitFilterKKOC shape (tensors.hpp:119-159). */
+typedef struct {
+  size_t kh, kw, out_channels, in_channels;
+  int tiled;
+  size_t bh, bw;
+} btnn_filter_desc;
+
+/* Conv2dGeometry (tensors.hpp:240-258). */
+typedef struct {
+  size_t kh, kw, stride, pad;
+} btnn_conv_geom;
+
+/* BnParams (layer_math.hpp:13-35): per-channel f64 arrays. */
+typedef struct {
+  const double *gamma, *beta, *mean, *var;
+  size_t channels;
+  double eps;
+} btnn_bn;
+
+/* ConvFused (bconv.hpp:152-158). Exactly one of (thresholds, bn). Residual tensors are
+ * RealTensorPQNO values, p*q*batch*o doubles; residual_out is overwritten. */
+typedef struct {
+  const double* tau;        /* Threshold::tau, n_thresholds entries (or NULL) */
+  const uint8_t* kind;      /* Threshold::kind */
+  size_t n_thresholds;
+  const btnn_bn* bn;        /* or NULL */
+  const double* residual_in;
+  double* residual_out;
+  int threads;
+} btnn_conv_fused;
+
+/* ---- library ---------------------------------------------------------------------- */
+int btnn_cuda_abi_version(void);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* btnn_cuda_last_error(void);
+int btnn_cuda_device_count(int* n);
+/* Device used by the kernel-level calls issued from this host thread (default 0). */
+int btnn_cuda_set_device(int device);
+
+/* ---- storage sizes (words of uint64) --------------------------------------------- */
+size_t btnn_cuda_matrix_words(const btnn_matrix_desc* d);     /* BitMatrix::storage_bits/64 */
+size_t btnn_cuda_act_words(const btnn_act_desc* d);           /* BitTensorHWNC bits */
+size_t btnn_cuda_filter_words(const btnn_filter_desc* d);     /* BitFilterKKOC bits */
+
+/* ---- format stage ---------------------------------------------------------------- */
+/* pack_matrix (bit_matrix.hpp:135-155): sign-binarize row-major floats (x >= 0 -> 1). */
+int btnn_cuda_pack_matrix(const float* values, size_t n_values, const btnn_matrix_desc* out_desc,
+                          uint64_t* out_words);
+/* pack_nhwc (tensors.hpp:162-174): NHWC floats -> HWNC bits. */
+int btnn_cuda_pack_nhwc(const float* x, size_t batch, size_t height, size_t width, size_t channels,
+                        int tiled, size_t bh, size_t bw, uint64_t* out_words);
+/* to_fsb / from_fsb (bit_matrix.hpp:224-253). out_desc gives the target geometry. */
+int btnn_cuda_to_fsb(const btnn_matrix_desc* src, const uint64_t* src_words, size_t bh, size_t bw,
+                     uint64_t* out_words);
+int btnn_cuda_from_fsb(const btnn_matrix_desc* src, const uint64_t* src_words, uint64_t* out_words);
+/* convert_activations (tensors.hpp:203-212). */
+int btnn_cuda_convert_activations(const btnn_act_desc* src, const uint64_t* src_words, int tiled,
+                                  size_t bh, size_t bw, uint64_t* out_words);
+/* flatten_to_matrix (tensors.hpp:226-237). */
+int btnn_cuda_flatten_to_matrix(const btnn_act_desc* src, const uint64_t* src_words,
+                                const btnn_matrix_desc* out_desc, uint64_t* out_words);
+
+/* ---- BMM (bmm.hpp:204-274) ------------------------------------------------------- */
+/* bmm_raw (bmm.hpp:204-214): out = xor-popcount accumulators, a.rows x b.cols int32. */
+int btnn_cuda_bmm_raw(const btnn_matrix_desc* a, const uint64_t* a_words, const btnn_matrix_desc* b,
+                      const uint64_t* b_words, const btnn_bmm_options* opt, int32_t* out);
+/* bmm_pm1 (bmm.hpp:219-228): out = n - 2*acc. */
+int btnn_cuda_bmm_pm1(const btnn_matrix_desc* a, const uint64_t* a_words, const btnn_matrix_desc* b,
+                      const uint64_t* b_words, const btnn_bmm_options* opt, int32_t* out);
+/* bmm_pm1_bin (bmm.hpp:256-274): thresholded bits; output layout follows A's family
+ * (RowPacked, or FsbRow with A's geometry). n_thresholds == 0 -> plain sign rule. */
+int btnn_cuda_bmm_pm1_bin(const btnn_matrix_desc* a, const uint64_t* a_words,
+                          const btnn_matrix_desc* b, const uint64_t* b_words,
+                          const btnn_bmm_options* opt, const double* tau, const uint8_t* kind,
+                          size_t n_thresholds, uint64_t* out_words);
+
+/* ---- BConv (bconv.hpp:138-272) --------------------------------------------------- */
+/* bconv_pm1 (bconv.hpp:138-146): IntTensorPQNO p*q*batch*o. */
+int btnn_cuda_bconv_pm1(const btnn_act_desc* in, const uint64_t* in_words, const btnn_filter_desc* f,
+                        const uint64_t* f_words, const btnn_conv_geom* geo, int32_t* out);
+/* bconv_fused (bconv.hpp:160-194): packed HWNC bits in the input's layout. */
+int btnn_cuda_bconv_fused(const btnn_act_desc* in, const uint64_t* in_words,
+                          const btnn_filter_desc* f, const uint64_t* f_words,
+                          const btnn_conv_geom* geo, const btnn_conv_fused* fused,
+                          uint64_t* out_words);
+/* first_conv_bwn (bconv.hpp:198-243): weights_pm1 is (o, r, s, c) ordered +-1 floats. */
+int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t width,
+                             size_t channels, const float* weights_pm1, size_t n_weights,
+                             size_t kh, size_t kw, size_t out_channels, const btnn_conv_geom* geo,
+                             double* out);
+/* or_pool (bconv.hpp:247-272). */
+int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t window,
+                      size_t stride, uint64_t* out_words);
+
+/* ---- model driver (inference.hpp:67-186) ----------------------------------------- */
+/* LayerSpec (model.hpp:36-52), already resolved (resolve_model, model.hpp:190-296). */
+typedef struct {
+  int kind;
+  size_t kh, kw, out_channels, stride, pad;
+  size_t window, pool_stride;
+  size_t units;
+  size_t in_h, in_w, in_channels;
+  size_t out_h, out_w;
+  int residual_out, residual_in, shortcut_from;
+} btnn_layer_spec;
+
+/* ModelSpec (model.hpp:58-65). */
+typedef struct {
+  const char* name;
+  size_t in_h, in_w, in_c, classes;
+  double epsilon;
+  const btnn_layer_spec* layers;
+  size_t n_layers;
+} btnn_model_spec;
+
+/* LayerWeights (weights.hpp:213-221), in the store's layout. */
+typedef struct {
+  int kind;
+  const uint64_t* filter_words; size_t filter_n_words;   /* conv kinds: BitFilterKKOC bits */
+  const float* conv_pm1; size_t conv_pm1_n;              /* first conv: (o,r,s,c) +-1 floats */
+  const uint64_t* fc_words; size_t fc_n_words;           /* fc kinds: BitMatrix in x out, ColPacked/FsbCol */
+  const double* tau; const uint8_t* tkind; size_t n_thresholds;
+  int has_bn;
+  btnn_bn bn;
+} btnn_layer_weights;
+
+/* WeightStore (weights.hpp:223-227). */
+typedef struct {
+  int tiled;
+  size_t bh, bw;
+  const btnn_layer_weights* layers;
+  size_t n_layers;
+} btnn_weight_store;
+
+typedef struct btnn_plan btnn_plan;
+
+/* Build a device plan: validate model/weights like run_inference (inference.hpp:69-75),
+ * convert weights to the device formats and upload them once to every listed device.
+ * max_batch bounds the per-call batch; the batch is sharded across the devices in
+ * contiguous chunks (one CUDA stream and one host thread per device). */
+int btnn_cuda_plan_create(const btnn_model_spec* model, const btnn_weight_store* ws, size_t max_batch,
+                          const int* devices, int n_devices, btnn_plan** out);
+/* run_inference (inference.hpp:67-186) on host buffers: x is NHWC f32 batch*H*W*C; logits
+ * batch*classes f64 and labels (first argmax) are written back. Synchronous. */
+int btnn_cuda_plan_run(btnn_plan* plan, const float* x, size_t batch, double* logits, int32_t* labels);
+/* Device-resident variant for shard `shard` (its own device): pointers are device
+ * pointers on that device; stream is a cudaStream_t (NULL = the plan's stream). Async. */
+int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size_t batch,
+                              double* d_logits, int32_t* d_labels, void* stream);
+/* Per-layer device time of the last plan_run on shard 0, ms (RunOptions::breakdown,
+ * inference.hpp:169-174). n_layers entries. */
+int btnn_cuda_plan_layer_ms(btnn_plan* plan, double* ms, size_t n_layers);
+/* Enable/disable per-layer timing (adds events; off by default). */
+int btnn_cuda_plan_set_breakdown(btnn_plan* plan, int enabled);
+/* Kernel launches per plan_run on one shard (for the bench's gpu_launches). */
+int btnn_cuda_plan_launches(btnn_plan* plan, size_t batch, size_t* launches);
+/* Name of the engine chosen for layer i ("tc_i8", "popc", "fp64", "orpool", ...). */
+const char* btnn_cuda_plan_layer_engine(btnn_plan* plan, size_t i);
+int btnn_cuda_plan_destroy(btnn_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BTNN_CUDA_H_ */

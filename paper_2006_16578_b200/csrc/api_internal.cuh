@@ -1,0 +1,67 @@
+// api_internal.cuh — glue shared by the C-ABI translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <new>
+#include <string>
+#include <vector>
+
+#include "btnn_cuda.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace btnn_gpu {
+
+void set_last_error(const std::string& m);
+
+// Runs fn, mapping exceptions to the C-ABI status codes.
+template <class Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    set_last_error("");
+    return BTNN_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed");
+    return BTNN_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return BTNN_CUDA_ERROR;
+  }
+}
+
+void check_matrix_desc(const btnn_matrix_desc* d);
+void check_act_desc(const btnn_act_desc* d);
+void check_filter_desc(const btnn_filter_desc* d);
+void check_bn(const btnn_bn& bn);
+size_t conv_out(size_t x, size_t k, size_t stride, size_t pad, bool height);
+void thresholds_to_int(const double* tau, const uint8_t* kind, size_t n, std::vector<long long>& lo,
+                       std::vector<long long>& hi);
+void bn_to_device_arrays(const btnn_bn& bn, std::vector<double>& packed);
+
+// Engine selection for one implicit GEMM. Auto picks the tensor-core path when the shape
+// and epilogue are covered by it and an expanded filter is available, else LOP3+POPC.
+enum class EngineHint { Auto, Popc, TcI8 };
+
+// Tensor-core operand prepared once per filter (see kernels_tc.cu): +-1 int8 expansion
+// of the filter in the UMMA canonical layout, plus per-(tap, o) logical weight sums.
+struct TcFilter {
+  DevBuf w8;        // int8 operand blocks
+  DevBuf wsum;      // int32 [taps][O]
+  int O = 0, O_pad = 0, taps = 0, kchunks = 0, n_tile = 0;
+  bool valid() const { return w8.get() != nullptr; }
+};
+
+// Returns the engine name used ("tc_i8" / "popc").
+const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e,
+                         cudaStream_t st, EngineHint h, const TcFilter* tc = nullptr);
+
+// Tensor-core support (kernels_tc.cu).
+bool tc_supported(const ConvShape& s, const Epi& e);
+void tc_prepare_filter(const ConvShape& s, const uint64_t* filt_plain, TcFilter& out, cudaStream_t st);
+void launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st);
+
+}  // namespace btnn_gpu

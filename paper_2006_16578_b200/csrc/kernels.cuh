@@ -1,0 +1,90 @@
+// kernels.cuh — launchers of the sm_100a kernels behind libbtnn_cuda.
+//
+// One implicit-GEMM description covers both hot functions of the paper: BConv over HWNC
+// activations x KKOC filters (bconv.hpp:76-133), and BMM as the 1x1, single-site special
+// case (A RowPacked rows = "images", B ColPacked columns = "output channels",
+// bmm.hpp:81-99). Every GEMM row is one output (site, n); every column one output channel.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace btnn_gpu {
+
+struct ConvShape {
+  int P, Q;              // output grid
+  int H, W;              // input grid
+  int KH, KW, stride, pad;
+  int N;                 // logical rows per site (batch); GEMM rows M = P*Q*N
+  int in_rps;            // input row pitch per site, in rows (n_pad)
+  int out_rps;           // output bit-tensor row pitch per site (n_pad)
+  int cw;                // u64 words per input row (c_pad / 64)
+  int C;                 // logical inner channels: v = C * valid_taps - 2 * acc
+  int O;                 // logical output channels
+  int f_rps;             // filter rows per tap plane (o_pad)
+  int cwo;               // u64 words per output bit row (out c_pad / 64)
+};
+
+// Fused epilogue (bconv.hpp:160-194, bmm.hpp:219-274, inference.hpp:107-118/161-164).
+enum EpiMode { EPI_I32 = 0, EPI_BITS = 1, EPI_F64 = 2 };
+struct Epi {
+  int mode = EPI_I32;
+  int raw = 0;                       // EPI_I32: write the raw xor-popcount (bmm_raw)
+  int32_t* out_i32 = nullptr;        // PQNO / row-major M x O
+  uint64_t* out_bits = nullptr;      // HWNC plain / RowPacked words (pre-zeroed)
+  const long long* thr_lo = nullptr; // threshold route: bit = lo <= v <= hi (per channel)
+  const long long* thr_hi = nullptr;
+  const double* bn_mean = nullptr;   // bn route: y = (v - mean) / s * gamma + beta
+  const double* bn_s = nullptr;      //   s = sqrt(var + eps), computed on the host in IEEE f64
+  const double* bn_gamma = nullptr;
+  const double* bn_beta = nullptr;
+  const double* rin = nullptr;       // residual_in, PQNO over (rin_P, rin_Q, N, rin_C)
+  int rin_P = 0, rin_Q = 0, rin_C = 0, rin_halve = 0;  // type-A adaptation (inference.hpp:43-63)
+  double* rout = nullptr;            // residual_out / logits, PQNO over (P, Q, N, O)
+};
+
+// CUDA-core LOP3+POPC implicit GEMM (any shape). act/filt are device pointers.
+void launch_bgemm_popc(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e,
+                       cudaStream_t st);
+
+// First layer (bconv.hpp:198-243 + inference.hpp:101-120): f64 (r,s,c)-ordered sums.
+struct FirstConvArgs {
+  const float* x;         // NHWC
+  const float* w_pm1;     // (o, r, s, c) +-1 floats
+  int N, H, W, C, O, KH, KW, stride, pad, P, Q;
+  double* out_acc;        // optional raw sums, PQNO (first_conv_bwn)
+  // optional fused bn -> tap -> sign -> HWNC bits (run_inference's loop)
+  const double *bn_mean, *bn_s, *bn_gamma, *bn_beta;
+  double* tap;            // optional, PQNO
+  uint64_t* out_bits;     // optional, HWNC plain (pre-zeroed)
+  int out_rps, cwo;
+};
+void launch_first_conv(const FirstConvArgs& a, cudaStream_t st);
+
+// Format stage.
+void launch_check_finite(const float* x, size_t n, int* flag, cudaStream_t st);
+// Sign-binarize a row-major rows x cols f32 matrix into a plain RowPacked bit matrix
+// (pack_matrix, bit_matrix.hpp:135-155). out pre-zeroed; row pitch in u32 words.
+void launch_pack_rows(const float* x, size_t rows, size_t cols, size_t row_words32, uint32_t* out,
+                      int* nonfinite, cudaStream_t st);
+// NHWC f32 -> plain HWNC bits (pack_nhwc, tensors.hpp:162-174). out pre-zeroed.
+void launch_pack_nhwc(const float* x, int N, int H, int W, int C, int n_pad, int c_pad, uint32_t* out,
+                      int* nonfinite, cudaStream_t st);
+// Generic matrix layout conversion (to_fsb/from_fsb/any), one thread per output word.
+void launch_convert_matrix(size_t rows, size_t cols, int src_layout, size_t sbh, size_t sbw,
+                           const uint64_t* src, int dst_layout, size_t dbh, size_t dbw, uint64_t* dst,
+                           cudaStream_t st);
+// Activation plane layout conversion (convert_activations, tensors.hpp:203-212).
+void launch_convert_act(size_t h, size_t w, size_t n, size_t c, int src_tiled, size_t sbh, size_t sbw,
+                        const uint64_t* src, int dst_tiled, size_t dbh, size_t dbw, uint64_t* dst,
+                        cudaStream_t st);
+// flatten_to_matrix (tensors.hpp:226-237) from plain HWNC to plain RowPacked.
+void launch_flatten(const uint64_t* act, int H, int W, int N, int C, int n_pad, int c_pad, uint64_t* out,
+                    size_t out_row_words, cudaStream_t st);
+// or_pool (bconv.hpp:247-272) over whole plane words.
+void launch_or_pool(const uint64_t* in, int H, int W, size_t plane_words, int window, int stride, int OH,
+                    int OW, uint64_t* out, cudaStream_t st);
+// First-index argmax over logits rows (inference.hpp:177-184).
+void launch_argmax(const double* logits, int batch, int classes, int32_t* labels, cudaStream_t st);
+
+}  // namespace btnn_gpu

@@ -1,0 +1,517 @@
+// plan.cu — the model driver: run_inference (inference.hpp:67-186) as a device plan.
+//
+// A plan holds, per device ("shard"), the weights converted once to the device formats,
+// the activation / tap / FC buffers sized for the shard's max batch, and a CUDA graph
+// per (batch, pointers) that replays the whole layer sequence. The batch is split into
+// contiguous per-device chunks; no sample couples to another (bn uses frozen statistics,
+// layer_math.hpp:32-34), so the shards need no collective and the result is identical
+// to a single-device run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "api_internal.cuh"
+#include "common.cuh"
+#include "kernels.cuh"
+#include "layout.cuh"
+
+namespace btnn_gpu {
+
+struct LayerDev {
+  btnn_layer_spec spec{};
+  DevBuf filt;          // plain KKOC filter / ColPacked fc matrix
+  TcFilter tc;          // tensor-core operand (bit conv / fc when covered)
+  DevBuf wpm1;          // first conv (o,r,s,c) floats
+  DevBuf thr_lo, thr_hi;
+  DevBuf bn;            // mean | s | gamma | beta
+  bool has_thr = false, has_bn = false;
+  DevBuf tap;           // residual_out, PQNO f64 sized for max batch
+  std::string engine = "-";
+};
+
+struct Shard {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  size_t max_batch = 0;
+  std::vector<LayerDev> layers;
+  DevBuf x, act[2], fc[2], logits, labels, flag;
+  size_t act_words = 0, fc_words = 0;
+  std::map<std::tuple<size_t, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
+  std::vector<cudaEvent_t> events;  // breakdown
+  size_t launches = 0;
+  ~Shard() {
+    if (device >= 0) cudaSetDevice(device);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto ev : events) cudaEventDestroy(ev);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+}  // namespace btnn_gpu
+
+struct btnn_plan {
+  std::string name;
+  size_t in_h = 0, in_w = 0, in_c = 0, classes = 0;
+  std::vector<btnn_layer_spec> specs;
+  std::vector<std::unique_ptr<btnn_gpu::Shard>> shards;
+  bool breakdown = false;
+  std::vector<double> layer_ms;
+};
+
+namespace btnn_gpu {
+
+static ConvShape conv_shape(const btnn_layer_spec& l, size_t batch) {
+  ConvShape s{};
+  s.P = (int)l.out_h; s.Q = (int)l.out_w;
+  s.H = (int)l.in_h; s.W = (int)l.in_w;
+  s.KH = (int)l.kh; s.KW = (int)l.kw; s.stride = (int)l.stride; s.pad = (int)l.pad;
+  s.N = (int)batch;
+  s.in_rps = s.out_rps = (int)act_npad(batch, 0, 0);
+  s.cw = (int)(act_cpad(l.in_channels, 0, 0) / 64);
+  s.C = (int)l.in_channels;
+  s.O = (int)l.out_channels;
+  s.f_rps = (int)filt_opad(l.out_channels, 0, 0);
+  s.cwo = (int)(act_cpad(l.out_channels, 0, 0) / 64);
+  return s;
+}
+
+static ConvShape fc_shape(const btnn_layer_spec& l, size_t batch) {
+  ConvShape s{};
+  s.P = s.Q = s.H = s.W = 1;
+  s.KH = s.KW = s.stride = 1;
+  s.pad = 0;
+  s.N = (int)batch;
+  s.in_rps = s.out_rps = (int)batch;
+  s.cw = (int)(ru(l.in_channels, 128) / 64);
+  s.C = (int)l.in_channels;
+  s.O = (int)l.units;
+  s.f_rps = (int)l.units;
+  s.cwo = (int)(ru(l.units, 128) / 64);
+  return s;
+}
+
+// Validation of the (model, store) pair; run_inference checks the layer count
+// (inference.hpp:69-70), the rest guards the raw C ABI against short buffers.
+static void check_plan_inputs(const btnn_model_spec* m, const btnn_weight_store* ws) {
+  require(m && ws && m->layers && ws->layers, BTNN_INVALID_INPUT, "plan: null model or weights");
+  require(ws->n_layers == m->n_layers, BTNN_INVALID_INPUT, "run_inference: weight store does not match model");
+  require(m->n_layers > 0, BTNN_VALIDATION_ERROR, "model: no layers");
+  if (ws->tiled)
+    require(ws->bh * ws->bw != 0 && (ws->bh * ws->bw) % 64 == 0 && ws->bw % 64 == 0, BTNN_UNSUPPORTED_SHAPE,
+            "plan: unsupported tile geometry");
+  for (size_t i = 0; i < m->n_layers; ++i) {
+    const btnn_layer_spec& l = m->layers[i];
+    const btnn_layer_weights& w = ws->layers[i];
+    const std::string tag = "layer " + std::to_string(i);
+    require(w.kind == l.kind, BTNN_VALIDATION_ERROR, tag + ": weight record kind does not match model");
+    const bool conv = l.kind == BTNN_FIRST_CONV_BWN || l.kind == BTNN_BIT_CONV;
+    const bool fc = l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC;
+    if (l.kind == BTNN_FIRST_CONV_BWN)
+      require(w.conv_pm1 && w.conv_pm1_n == l.kh * l.kw * l.out_channels * l.in_channels, BTNN_VALIDATION_ERROR,
+              tag + ": first conv weights missing");
+    if (l.kind == BTNN_BIT_CONV)
+      require(w.filter_words &&
+                  w.filter_n_words == filt_words(l.kh, l.kw, l.out_channels, l.in_channels, ws->tiled, ws->bh, ws->bw),
+              BTNN_VALIDATION_ERROR, tag + ": filter word count does not match");
+    if (fc)
+      require(w.fc_words && w.fc_n_words == mat_words(l.in_channels, l.units, ws->tiled ? BTNN_FSB_COL : BTNN_COL_PACKED,
+                                                      ws->bh, ws->bw),
+              BTNN_VALIDATION_ERROR, tag + ": fc word count does not match");
+    const size_t outc = conv ? l.out_channels : (fc ? l.units : 0);
+    const bool bn_route = l.kind == BTNN_FIRST_CONV_BWN || l.kind == BTNN_LAST_FC || l.residual_in || l.residual_out;
+    if (l.kind != BTNN_OR_POOL) {
+      if (bn_route || w.n_thresholds == 0) {
+        require(w.has_bn && w.bn.channels == outc, BTNN_VALIDATION_ERROR, tag + ": bn parameters missing");
+        check_bn(w.bn);
+      } else {
+        require(w.n_thresholds == outc && w.tau && w.tkind, BTNN_VALIDATION_ERROR, tag + ": threshold count does not match");
+      }
+    }
+    if (l.residual_in)
+      require(l.shortcut_from >= 0 && (size_t)l.shortcut_from < i && m->layers[l.shortcut_from].residual_out,
+              BTNN_VALIDATION_ERROR, tag + ": bad shortcut source");
+  }
+}
+
+static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_store* ws) {
+  BT_CUDA(cudaSetDevice(sh.device));
+  BT_CUDA(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+  cudaStream_t st = sh.stream;
+  const size_t B = sh.max_batch;
+  sh.layers.resize(m->n_layers);
+  size_t act_max = 1, fc_max = 1;
+  for (size_t i = 0; i < m->n_layers; ++i) {
+    const btnn_layer_spec& l = m->layers[i];
+    const btnn_layer_weights& w = ws->layers[i];
+    LayerDev& L = sh.layers[i];
+    L.spec = l;
+    if (l.kind == BTNN_FIRST_CONV_BWN || l.kind == BTNN_BIT_CONV || l.kind == BTNN_OR_POOL)
+      act_max = std::max(act_max, act_words(l.out_h, l.out_w, B, l.out_channels, 0, 0, 0));
+    if (l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC) {
+      fc_max = std::max(fc_max, B * ru(l.in_channels, 128) / 64);
+      fc_max = std::max(fc_max, B * ru(l.units, 128) / 64);
+    }
+    if (l.kind == BTNN_FIRST_CONV_BWN) {
+      L.wpm1 = upload(w.conv_pm1, w.conv_pm1_n, st);
+    } else if (l.kind == BTNN_BIT_CONV) {
+      DevBuf raw = upload(w.filter_words, w.filter_n_words, st);
+      if (!ws->tiled) {
+        L.filt = std::move(raw);
+      } else {
+        L.filt.alloc(filt_words(l.kh, l.kw, l.out_channels, l.in_channels, 0, 0, 0) * 8);
+        launch_convert_act(l.kh, l.kw, l.out_channels, l.in_channels, 1, ws->bh, ws->bw, raw.get<uint64_t>(), 0, 0, 0,
+                           L.filt.get<uint64_t>(), st);
+        BT_CUDA(cudaStreamSynchronize(st));
+      }
+      tc_prepare_filter(conv_shape(l, B), L.filt.get<uint64_t>(), L.tc, st);
+    } else if (l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC) {
+      DevBuf raw = upload(w.fc_words, w.fc_n_words, st);
+      if (!ws->tiled) {
+        L.filt = std::move(raw);
+      } else {
+        L.filt.alloc(mat_words(l.in_channels, l.units, BTNN_COL_PACKED, 0, 0) * 8);
+        launch_convert_matrix(l.in_channels, l.units, BTNN_FSB_COL, ws->bh, ws->bw, raw.get<uint64_t>(),
+                              BTNN_COL_PACKED, 0, 0, L.filt.get<uint64_t>(), st);
+        BT_CUDA(cudaStreamSynchronize(st));
+      }
+      tc_prepare_filter(fc_shape(l, B), L.filt.get<uint64_t>(), L.tc, st);
+    }
+    if (l.kind != BTNN_OR_POOL) {
+      if (w.n_thresholds && !(l.kind == BTNN_LAST_FC || l.kind == BTNN_FIRST_CONV_BWN || l.residual_in || l.residual_out)) {
+        std::vector<long long> lo, hi;
+        thresholds_to_int(w.tau, w.tkind, w.n_thresholds, lo, hi);
+        L.thr_lo = upload(lo.data(), lo.size(), st);
+        L.thr_hi = upload(hi.data(), hi.size(), st);
+        L.has_thr = true;
+      } else {
+        std::vector<double> p;
+        bn_to_device_arrays(w.bn, p);
+        L.bn = upload(p.data(), p.size(), st);
+        L.has_bn = true;
+      }
+    }
+    if (l.residual_out) L.tap.alloc(l.out_h * l.out_w * B * l.out_channels * sizeof(double));
+    BT_CUDA(cudaStreamSynchronize(st));  // host staging vectors die here
+  }
+  sh.act_words = act_max;
+  sh.fc_words = fc_max;
+  for (auto& a : sh.act) a.alloc(act_max * 8);
+  for (auto& f : sh.fc) f.alloc(fc_max * 8);
+  sh.x.alloc(B * m->in_h * m->in_w * m->in_c * sizeof(float));
+  sh.logits.alloc(B * m->classes * sizeof(double));
+  sh.labels.alloc(B * sizeof(int32_t));
+  sh.flag.alloc(sizeof(int));
+  sh.events.resize(m->n_layers + 1);
+  for (auto& ev : sh.events) BT_CUDA(cudaEventCreate(&ev));
+  BT_CUDA(cudaStreamSynchronize(st));
+}
+
+// Enqueues the whole layer sequence for `batch` samples of x (device) on the shard's
+// stream. Returns the number of kernels launched.
+static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size_t batch, double* d_logits,
+                              int32_t* d_labels, bool timed) {
+  cudaStream_t st = sh.stream;
+  size_t launches = 0;
+  BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), st));
+  launch_check_finite(d_x, batch * plan->in_h * plan->in_w * plan->in_c, sh.flag.get<int>(), st);
+  ++launches;
+  const size_t np = act_npad(batch, 0, 0);
+  int cur = 0;              // act buffer holding the current activations
+  int fcur = 0;             // fc buffer holding the current fc activations
+  bool in_fc = false;
+  size_t H = plan->in_h, W = plan->in_w, C = plan->in_c;
+  for (size_t i = 0; i < sh.layers.size(); ++i) {
+    LayerDev& L = sh.layers[i];
+    const btnn_layer_spec& l = L.spec;
+    if (timed) BT_CUDA(cudaEventRecord(sh.events[i], st));
+    if (l.kind == BTNN_FIRST_CONV_BWN) {
+      uint64_t* out = sh.act[cur].get<uint64_t>();
+      BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
+      FirstConvArgs a{};
+      a.x = d_x;
+      a.w_pm1 = L.wpm1.get<float>();
+      a.N = (int)batch; a.H = (int)l.in_h; a.W = (int)l.in_w; a.C = (int)l.in_channels; a.O = (int)l.out_channels;
+      a.KH = (int)l.kh; a.KW = (int)l.kw; a.stride = (int)l.stride; a.pad = (int)l.pad;
+      a.P = (int)l.out_h; a.Q = (int)l.out_w;
+      const size_t C4 = l.out_channels;
+      a.bn_mean = L.bn.get<double>(); a.bn_s = a.bn_mean + C4; a.bn_gamma = a.bn_mean + 2 * C4; a.bn_beta = a.bn_mean + 3 * C4;
+      a.tap = l.residual_out ? L.tap.get<double>() : nullptr;
+      a.out_bits = out;
+      a.out_rps = (int)np;
+      a.cwo = (int)(act_cpad(l.out_channels, 0, 0) / 64);
+      launch_first_conv(a, st);
+      ++launches;
+      L.engine = "fp64";
+      H = l.out_h; W = l.out_w; C = l.out_channels;
+    } else if (l.kind == BTNN_BIT_CONV) {
+      const uint64_t* in = sh.act[cur].get<uint64_t>();
+      uint64_t* out = sh.act[cur ^ 1].get<uint64_t>();
+      BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
+      const ConvShape s = conv_shape(l, batch);
+      Epi e;
+      e.mode = EPI_BITS;
+      e.out_bits = out;
+      if (L.has_thr) {
+        e.thr_lo = L.thr_lo.get<long long>();
+        e.thr_hi = L.thr_hi.get<long long>();
+      } else {
+        const size_t O = l.out_channels;
+        e.bn_mean = L.bn.get<double>(); e.bn_s = e.bn_mean + O; e.bn_gamma = e.bn_mean + 2 * O; e.bn_beta = e.bn_mean + 3 * O;
+      }
+      if (l.residual_in) {
+        const LayerDev& src = sh.layers[l.shortcut_from];
+        e.rin = src.tap.get<double>();
+        e.rin_P = (int)src.spec.out_h;
+        e.rin_Q = (int)src.spec.out_w;
+        e.rin_C = (int)src.spec.out_channels;
+        e.rin_halve = src.spec.out_h != l.out_h;  // adapt_shortcut's `halve` (inference.hpp:46)
+      }
+      if (l.residual_out) e.rout = L.tap.get<double>();
+      L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
+      ++launches;
+      cur ^= 1;
+      H = l.out_h; W = l.out_w; C = l.out_channels;
+    } else if (l.kind == BTNN_OR_POOL) {
+      const size_t pw = np * act_cpad(C, 0, 0) / 64;
+      launch_or_pool(sh.act[cur].get<uint64_t>(), (int)H, (int)W, pw, (int)l.window, (int)l.pool_stride, (int)l.out_h,
+                     (int)l.out_w, sh.act[cur ^ 1].get<uint64_t>(), st);
+      ++launches;
+      L.engine = "orpool";
+      cur ^= 1;
+      H = l.out_h; W = l.out_w;
+    } else {
+      if (!in_fc) {
+        uint64_t* dst = sh.fc[fcur].get<uint64_t>();
+        const size_t row_words = ru(l.in_channels, 128) / 64;
+        if (i == 0) {
+          // FC-first model: binarize the raw input (inference.hpp:149-151); non-finite
+          // values were already flagged by the input check.
+          BT_CUDA(cudaMemsetAsync(dst, 0, batch * row_words * 8, st));
+          launch_pack_rows(d_x, batch, l.in_channels, row_words * 2, reinterpret_cast<uint32_t*>(dst),
+                           sh.flag.get<int>(), st);
+        } else {
+          launch_flatten(sh.act[cur].get<uint64_t>(), (int)H, (int)W, (int)batch, (int)C, (int)np,
+                         (int)act_cpad(C, 0, 0), dst, row_words, st);
+        }
+        ++launches;
+        in_fc = true;
+      }
+      const ConvShape s = fc_shape(l, batch);
+      Epi e;
+      if (l.kind == BTNN_BIT_FC) {
+        uint64_t* out = sh.fc[fcur ^ 1].get<uint64_t>();
+        BT_CUDA(cudaMemsetAsync(out, 0, batch * (size_t)s.cwo * 8, st));
+        e.mode = EPI_BITS;
+        e.out_bits = out;
+        e.thr_lo = L.thr_lo.get<long long>();
+        e.thr_hi = L.thr_hi.get<long long>();
+        L.engine = launch_bgemm(s, sh.fc[fcur].get<uint64_t>(), L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
+        fcur ^= 1;
+      } else {
+        const size_t O = l.units;
+        e.mode = EPI_F64;
+        e.bn_mean = L.bn.get<double>(); e.bn_s = e.bn_mean + O; e.bn_gamma = e.bn_mean + 2 * O; e.bn_beta = e.bn_mean + 3 * O;
+        e.rout = d_logits;  // logits = bn(v) (inference.hpp:161-164)
+        L.engine = launch_bgemm(s, sh.fc[fcur].get<uint64_t>(), L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
+      }
+      ++launches;
+    }
+  }
+  if (timed) BT_CUDA(cudaEventRecord(sh.events[sh.layers.size()], st));
+  launch_argmax(d_logits, (int)batch, (int)plan->classes, d_labels, st);
+  ++launches;
+  return launches;
+}
+
+// Enqueue via a cached CUDA graph (or eagerly when timing layers).
+static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_t batch, double* d_logits,
+                             int32_t* d_labels, bool timed) {
+  if (timed) {
+    sh.launches = enqueue_forward(plan, sh, d_x, batch, d_logits, d_labels, true);
+    return;
+  }
+  auto key = std::make_tuple(batch, (const void*)d_x, (const void*)d_logits, (const void*)d_labels);
+  auto it = sh.graphs.find(key);
+  if (it == sh.graphs.end()) {
+    cudaGraph_t g;
+    BT_CUDA(cudaStreamBeginCapture(sh.stream, cudaStreamCaptureModeThreadLocal));
+    size_t n = 0;
+    try {
+      n = enqueue_forward(plan, sh, d_x, batch, d_logits, d_labels, false);
+    } catch (...) {
+      cudaStreamEndCapture(sh.stream, &g);
+      throw;
+    }
+    BT_CUDA(cudaStreamEndCapture(sh.stream, &g));
+    cudaGraphExec_t ex;
+    BT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    sh.launches = n;
+    it = sh.graphs.emplace(key, ex).first;
+  }
+  BT_CUDA(cudaGraphLaunch(it->second, sh.stream));
+}
+
+static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t batch, double* logits, int32_t* labels) {
+  BT_CUDA(cudaSetDevice(sh.device));
+  const size_t xin = batch * plan->in_h * plan->in_w * plan->in_c;
+  BT_CUDA(cudaMemcpyAsync(sh.x.get(), x, xin * sizeof(float), cudaMemcpyHostToDevice, sh.stream));
+  run_shard_device(plan, sh, sh.x.get<float>(), batch, sh.logits.get<double>(), sh.labels.get<int32_t>(),
+                   plan->breakdown && &sh == plan->shards[0].get());
+  int bad = 0;
+  BT_CUDA(cudaMemcpyAsync(&bad, sh.flag.get(), sizeof(int), cudaMemcpyDeviceToHost, sh.stream));
+  BT_CUDA(cudaMemcpyAsync(logits, sh.logits.get(), batch * plan->classes * sizeof(double), cudaMemcpyDeviceToHost,
+                          sh.stream));
+  BT_CUDA(cudaMemcpyAsync(labels, sh.labels.get(), batch * sizeof(int32_t), cudaMemcpyDeviceToHost, sh.stream));
+  BT_CUDA(cudaStreamSynchronize(sh.stream));
+  require(!bad, BTNN_INVALID_INPUT, "run_inference: non-finite input");
+  if (plan->breakdown && &sh == plan->shards[0].get()) {
+    plan->layer_ms.assign(sh.layers.size(), 0.0);
+    for (size_t i = 0; i < sh.layers.size(); ++i) {
+      float ms = 0.f;
+      BT_CUDA(cudaEventElapsedTime(&ms, sh.events[i], sh.events[i + 1]));
+      plan->layer_ms[i] = ms;
+    }
+  }
+}
+
+}  // namespace btnn_gpu
+
+using namespace btnn_gpu;
+
+extern "C" {
+
+int btnn_cuda_plan_create(const btnn_model_spec* m, const btnn_weight_store* ws, size_t max_batch, const int* devices,
+                          int n_devices, btnn_plan** out) {
+  return guard([&] {
+    require(out != nullptr, BTNN_INVALID_INPUT, "plan_create: null out");
+    *out = nullptr;
+    check_plan_inputs(m, ws);
+    require(max_batch > 0, BTNN_INVALID_INPUT, "plan_create: zero max_batch");
+    int count = 0;
+    BT_CUDA(cudaGetDeviceCount(&count));
+    std::vector<int> devs;
+    if (devices && n_devices > 0)
+      devs.assign(devices, devices + n_devices);
+    else
+      devs.push_back(0);
+    for (int d : devs) require(d >= 0 && d < count, BTNN_INVALID_INPUT, "plan_create: no such device");
+    auto plan = std::make_unique<btnn_plan>();
+    plan->name = m->name ? m->name : "";
+    plan->in_h = m->in_h; plan->in_w = m->in_w; plan->in_c = m->in_c; plan->classes = m->classes;
+    plan->specs.assign(m->layers, m->layers + m->n_layers);
+    const size_t per = cdiv(max_batch, devs.size());
+    for (int d : devs) {
+      auto sh = std::make_unique<Shard>();
+      sh->device = d;
+      sh->max_batch = per;
+      build_shard(*sh, m, ws);
+      plan->shards.push_back(std::move(sh));
+    }
+    *out = plan.release();
+  });
+}
+
+int btnn_cuda_plan_run(btnn_plan* plan, const float* x, size_t batch, double* logits, int32_t* labels) {
+  return guard([&] {
+    require(plan != nullptr, BTNN_INVALID_INPUT, "plan_run: null plan");
+    require(batch > 0, BTNN_INVALID_INPUT, "run_inference: empty batch");
+    const size_t n = plan->shards.size();
+    const size_t per = cdiv(batch, n);
+    require(per <= plan->shards[0]->max_batch, BTNN_INVALID_INPUT, "plan_run: batch exceeds the plan's max_batch");
+    const size_t xin = plan->in_h * plan->in_w * plan->in_c;
+    std::vector<int> codes(n, BTNN_OK);
+    std::vector<std::string> msgs(n);
+    auto work = [&](size_t k) {
+      const size_t b0 = k * per;
+      if (b0 >= batch) return;
+      const size_t bn = std::min(per, batch - b0);
+      try {
+        run_shard_host(plan, *plan->shards[k], x + b0 * xin, bn, logits + b0 * plan->classes, labels + b0);
+      } catch (const Error& e) {
+        codes[k] = e.code;
+        msgs[k] = e.what();
+      } catch (const std::exception& e) {
+        codes[k] = BTNN_CUDA_ERROR;
+        msgs[k] = e.what();
+      }
+    };
+    if (n == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (size_t k = 0; k < n; ++k) th.emplace_back(work, k);
+      for (auto& t : th) t.join();
+    }
+    // Report the lowest-numbered failing code (invalid input beats device errors).
+    int best = BTNN_OK;
+    std::string msg;
+    for (size_t k = 0; k < n; ++k)
+      if (codes[k] != BTNN_OK && (best == BTNN_OK || codes[k] < best)) { best = codes[k]; msg = msgs[k]; }
+    if (best != BTNN_OK) fail(best, msg);
+  });
+}
+
+int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size_t batch, double* d_logits,
+                              int32_t* d_labels, void* stream) {
+  return guard([&] {
+    require(plan && shard >= 0 && (size_t)shard < plan->shards.size(), BTNN_INVALID_INPUT, "plan_run_device: bad shard");
+    Shard& sh = *plan->shards[shard];
+    require(batch > 0 && batch <= sh.max_batch, BTNN_INVALID_INPUT, "plan_run_device: batch out of range");
+    BT_CUDA(cudaSetDevice(sh.device));
+    cudaStream_t user = static_cast<cudaStream_t>(stream);
+    cudaEvent_t ev;
+    if (user) {  // order the plan stream after the caller's stream
+      BT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      BT_CUDA(cudaEventRecord(ev, user));
+      BT_CUDA(cudaStreamWaitEvent(sh.stream, ev, 0));
+    }
+    run_shard_device(plan, sh, d_x, batch, d_logits ? d_logits : sh.logits.get<double>(),
+                     d_labels ? d_labels : sh.labels.get<int32_t>(), false);
+    if (user) {
+      BT_CUDA(cudaEventRecord(ev, sh.stream));
+      BT_CUDA(cudaStreamWaitEvent(user, ev, 0));
+      BT_CUDA(cudaEventDestroy(ev));
+    }
+  });
+}
+
+int btnn_cuda_plan_layer_ms(btnn_plan* plan, double* ms, size_t n_layers) {
+  return guard([&] {
+    require(plan && n_layers == plan->specs.size(), BTNN_INVALID_INPUT, "plan_layer_ms: size mismatch");
+    for (size_t i = 0; i < n_layers; ++i) ms[i] = i < plan->layer_ms.size() ? plan->layer_ms[i] : 0.0;
+  });
+}
+
+int btnn_cuda_plan_set_breakdown(btnn_plan* plan, int enabled) {
+  return guard([&] {
+    require(plan != nullptr, BTNN_INVALID_INPUT, "null plan");
+    plan->breakdown = enabled != 0;
+  });
+}
+
+int btnn_cuda_plan_launches(btnn_plan* plan, size_t batch, size_t* launches) {
+  return guard([&] {
+    require(plan != nullptr, BTNN_INVALID_INPUT, "null plan");
+    (void)batch;
+    *launches = plan->shards[0]->launches;
+  });
+}
+
+const char* btnn_cuda_plan_layer_engine(btnn_plan* plan, size_t i) {
+  if (!plan || plan->shards.empty() || i >= plan->shards[0]->layers.size()) return "";
+  return plan->shards[0]->layers[i].engine.c_str();
+}
+
+int btnn_cuda_plan_destroy(btnn_plan* plan) {
+  return guard([&] { delete plan; });
+}
+
+}  // extern "C"

@@ -1,0 +1,206 @@
+"""GPU parity of the kernel-level C ABI: every output bit-exact against the reference's
+golden fixtures and the C oracle, plus random sweeps in the style of acceptance.cpp
+criteria 1, 2 and 6, and the reference's error classes."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from fixtures import indices, load
+from oracle_lib import oracle, ptr
+from paper_2006_16578_b200 import btnn as B
+from paper_2006_16578_b200 import capi
+from paper_2006_16578_b200 import weights as Wt
+
+pytestmark = pytest.mark.gpu
+
+
+def md(r, c, lay, bh=8, bw=128):
+    return capi.MatrixDesc(int(r), int(c), lay, bh, bw)
+
+
+@pytest.mark.parametrize("i", indices(load("bmm"), "s", "shape"))
+def test_bmm_golden(i):
+    d = load("bmm")
+    m, n, k = (int(v) for v in d[f"s{i}_shape"])
+    da, db = md(m, n, capi.ROW_PACKED), md(n, k, capi.COL_PACKED)
+    A, Bw = d[f"s{i}_A"], d[f"s{i}_B"]
+    for variant in (capi.BMM_NAIVE, capi.BMM_BLOCKED):
+        assert np.array_equal(B.bmm_pm1(da, A, db, Bw, variant).reshape(-1), d[f"s{i}_pm1"])
+    if f"s{i}_raw" in d:
+        assert np.array_equal(B.bmm_raw(da, A, db, Bw).reshape(-1), d[f"s{i}_raw"])
+    assert np.array_equal(B.bmm_pm1_bin(da, A, db, Bw), d[f"s{i}_bin"])
+    assert np.array_equal(B.bmm_pm1_bin(da, A, db, Bw, tau=d[f"s{i}_tau"], kind=d[f"s{i}_kind"]), d[f"s{i}_bin_thr"])
+    got = B.bmm_pm1_bin(md(m, n, capi.FSB_ROW), d[f"s{i}_Afsb"], md(n, k, capi.FSB_COL), d[f"s{i}_Bfsb"], capi.BMM_FSB,
+                        tau=d[f"s{i}_tau"], kind=d[f"s{i}_kind"])
+    assert np.array_equal(got, d[f"s{i}_bin_fsb"])
+
+
+def test_bmm_random_sweep_vs_oracle():  # acceptance.cpp criterion 1 (600 cases) in reduced form
+    rng = np.random.default_rng(101)
+    for case in range(120):
+        m, n, k = (int(v) for v in rng.integers(1, 300, 3))
+        if case % 10 == 0:
+            n = int(rng.integers(1, 8)) * 128
+        fa, fb = rng.standard_normal(m * n, dtype=np.float32), rng.standard_normal(n * k, dtype=np.float32)
+        A, Bw = Wt.pack_matrix(fa, m, n, capi.ROW_PACKED), Wt.pack_matrix(fb, n, k, capi.COL_PACKED)
+        da, db = md(m, n, capi.ROW_PACKED), md(n, k, capi.COL_PACKED)
+        want = np.zeros(m * k, dtype=np.int32)
+        oracle().bo_bmm_pm1(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64), capi.BMM_NAIVE,
+                            ptr(want, C.c_int32))
+        got = B.bmm_pm1(da, A, db, Bw).reshape(-1)
+        assert np.array_equal(got, want), (m, n, k)
+        dense = np.where(fa >= 0, 1, -1).reshape(m, n) @ np.where(fb >= 0, 1, -1).reshape(n, k)
+        assert np.array_equal(got, dense.reshape(-1).astype(np.int32))
+
+
+def test_bmm_1024_cube():
+    """The BASELINE config: 1024^3 on random packed words (bench.hpp:76-87), vs the oracle."""
+    rng = np.random.default_rng(1)
+    A = rng.integers(0, 2**64, 1024 * 16, dtype=np.uint64)
+    Bw = rng.integers(0, 2**64, 1024 * 16, dtype=np.uint64)
+    da, db = md(1024, 1024, capi.ROW_PACKED), md(1024, 1024, capi.COL_PACKED)
+    want = np.zeros(1024 * 1024, dtype=np.int32)
+    oracle().bo_bmm_pm1(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64), capi.BMM_NAIVE,
+                        ptr(want, C.c_int32))
+    assert np.array_equal(B.bmm_pm1(da, A, db, Bw).reshape(-1), want)
+    raw = B.bmm_raw(da, A, db, Bw).reshape(-1)
+    assert np.array_equal(1024 - 2 * raw, want)
+
+
+@pytest.mark.parametrize("i", indices(load("bconv"), "c", "case"))
+def test_bconv_golden(i):
+    d = load("bconv")
+    h, w, n, c, o, k, s, pd = (int(v) for v in d[f"c{i}_case"])
+    g = capi.ConvGeom(k, k, s, pd)
+    bn = tuple(d[f"c{i}_bn"])
+    for tiled, t in ((0, "p"), (1, "t")):
+        ad, fd = capi.ActDesc(h, w, n, c, tiled, 8, 128), capi.FilterDesc(k, k, o, c, tiled, 8, 128)
+        aw, fw = d[f"c{i}_{t}_act"], d[f"c{i}_{t}_filt"]
+        assert np.array_equal(B.bconv_pm1(ad, aw, fd, fw, g), d[f"c{i}_pm1"]), t
+        bits, _ = B.bconv_fused(ad, aw, fd, fw, g, tau=d[f"c{i}_tau"], kind=d[f"c{i}_kind"])
+        assert np.array_equal(bits, d[f"c{i}_{t}_bits_thr"]), t
+        bits, rout = B.bconv_fused(ad, aw, fd, fw, g, bn=bn, residual_in=d[f"c{i}_rin"], want_residual_out=True)
+        assert np.array_equal(bits, d[f"c{i}_{t}_bits_bn"]), t
+        assert np.array_equal(rout.view(np.uint64), d[f"c{i}_{t}_rout"].view(np.uint64)), t
+
+
+def test_bconv_random_sweep_vs_oracle():  # acceptance.cpp criterion 2 (K, stride, pad sweep)
+    rng = np.random.default_rng(202)
+    for case in range(60):
+        k = int(rng.choice([1, 3, 5, 7, 11]))
+        s = int(rng.choice([1, 2, 4]))
+        pd = int(rng.choice([0, 1, 2, 5]))
+        h = int(rng.integers(max(1, k - 2 * pd), 16))
+        w = int(rng.integers(max(1, k - 2 * pd), 16))
+        n, c, o = int(rng.integers(1, 6)), int(rng.integers(1, 200)), int(rng.integers(1, 80))
+        x = rng.standard_normal((n, h, w, c), dtype=np.float32)
+        wt = rng.standard_normal(k * k * o * c, dtype=np.float32)
+        aw, fw = Wt.pack_nhwc(x), Wt.pack_filter(wt, k, k, o, c)
+        ad, fd, g = capi.ActDesc(h, w, n, c, 0, 8, 128), capi.FilterDesc(k, k, o, c, 0, 8, 128), capi.ConvGeom(k, k, s, pd)
+        P, Q = (h + 2 * pd - k) // s + 1, (w + 2 * pd - k) // s + 1
+        want = np.zeros(P * Q * n * o, dtype=np.int32)
+        assert oracle().bo_bconv_pm1(C.byref(ad), ptr(aw, C.c_uint64), C.byref(fd), ptr(fw, C.c_uint64), C.byref(g),
+                                     ptr(want, C.c_int32)) == 0
+        assert np.array_equal(B.bconv_pm1(ad, aw, fd, fw, g), want), (h, w, n, c, o, k, s, pd)
+
+
+def test_bconv_corner_excludes():  # test_bconv.cpp:74-86
+    c = 96
+    aw = Wt.pack_nhwc(np.ones((1, 6, 6, c), np.float32))
+    fw = Wt.pack_filter(np.ones(3 * 3 * 2 * c, np.float32), 3, 3, 2, c)
+    v = B.bconv_pm1(capi.ActDesc(6, 6, 1, c, 0, 8, 128), aw, capi.FilterDesc(3, 3, 2, c, 0, 8, 128),
+                    fw, capi.ConvGeom(3, 3, 1, 1)).reshape(6, 6, 1, 2)
+    assert v[0, 0, 0, 0] == 4 * c and v[0, 1, 0, 0] == 6 * c and v[1, 1, 0, 0] == 9 * c
+
+
+def test_first_conv_and_pool_golden():
+    d = load("first_conv_pool")
+    for i in indices(d, "f", "case"):
+        n, h, w, c, o, k, s, pd = (int(v) for v in d[f"f{i}_case"])
+        y = B.first_conv_bwn(d[f"f{i}_x"].reshape(n, h, w, c), d[f"f{i}_w"], k, k, o, capi.ConvGeom(k, k, s, pd))
+        assert np.array_equal(y.view(np.uint64), d[f"f{i}_y"].view(np.uint64)), i
+    for i in indices(d, "p", "case"):
+        h, w, n, c, win, st, tiled = (int(v) for v in d[f"p{i}_case"])
+        out = B.or_pool(capi.ActDesc(h, w, n, c, tiled, 8, 128), d[f"p{i}_in"], win, st)
+        assert np.array_equal(out, d[f"p{i}_out"]), i
+
+
+def test_format_stage_vs_harness_packers():
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((3, 5, 7, 130), dtype=np.float32)
+    x[0, 0, 0, :4] = [0.0, -0.0, 1.0, -1.0]
+    for tiled in (False, True):
+        assert np.array_equal(B.pack_nhwc(x, tiled), Wt.pack_nhwc(x, tiled))
+    v = rng.standard_normal(17 * 300, dtype=np.float32)
+    for lay in range(4):
+        assert np.array_equal(B.pack_matrix(v, 17, 300, lay), Wt.pack_matrix(v, 17, 300, lay)), lay
+    A = Wt.pack_matrix(v, 17, 300, capi.ROW_PACKED)
+    for geo in ((8, 128), (4, 64), (2, 256), (16, 128)):  # test_bitcore.cpp:168-183 round trips
+        f = B.to_fsb(md(17, 300, capi.ROW_PACKED), A, *geo)
+        assert np.array_equal(f, Wt.pack_matrix(v, 17, 300, capi.FSB_ROW, *geo))
+        assert np.array_equal(B.from_fsb(md(17, 300, capi.FSB_ROW, *geo), f), A)
+    ad = capi.ActDesc(5, 7, 3, 130, 0, 8, 128)
+    aw = Wt.pack_nhwc(x)
+    assert np.array_equal(B.convert_activations(ad, aw, True), Wt.pack_nhwc(x, True))
+    flat = x.reshape(3, -1)
+    assert np.array_equal(B.flatten_to_matrix(ad, aw, capi.ROW_PACKED), Wt.pack_matrix(flat, 3, flat.shape[1], capi.ROW_PACKED))
+    bad = x.copy()
+    bad[1, 2, 3, 4] = np.nan
+    with pytest.raises(capi.BtnnError) as e:
+        B.pack_nhwc(bad)
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+
+
+def test_fused_equals_unfused():  # acceptance.cpp criterion 6 in reduced form
+    rng = np.random.default_rng(66)
+    for case in range(20):
+        h = w = int(rng.integers(3, 12))
+        n, c, o = int(rng.integers(1, 9)), int(rng.integers(1, 300)), int(rng.integers(1, 130))
+        k, s = int(rng.choice([1, 3, 5])), int(rng.choice([1, 2]))
+        pd = k // 2
+        x = rng.standard_normal((n, h, w, c), dtype=np.float32)
+        wt = rng.standard_normal(k * k * o * c, dtype=np.float32)
+        ad, fd, g = capi.ActDesc(h, w, n, c, 0, 8, 128), capi.FilterDesc(k, k, o, c, 0, 8, 128), capi.ConvGeom(k, k, s, pd)
+        aw, fw = Wt.pack_nhwc(x), Wt.pack_filter(wt, k, k, o, c)
+        P, Q = (h + 2 * pd - k) // s + 1, (w + 2 * pd - k) // s + 1
+        v = B.bconv_pm1(ad, aw, fd, fw, g).reshape(P, Q, n, o)
+        gamma, beta = rng.standard_normal(o), rng.standard_normal(o)
+        mean, var = rng.standard_normal(o) * 5, rng.uniform(0.25, 2.0, o)
+        tau, kind = Wt.fold_bn_sign(gamma, beta, mean, var, 1e-5)
+        bits, _ = B.bconv_fused(ad, aw, fd, fw, g, tau=tau, kind=kind)
+        want = Wt.bn_apply(v, gamma, beta, mean, var, 1e-5) >= 0
+        got = Wt.unpack_act(bits, P, Q, n, o)
+        assert np.array_equal(got.transpose(0, 1, 2, 3), want)
+        rin = rng.standard_normal(P * Q * n * o)
+        bits2, rout = B.bconv_fused(ad, aw, fd, fw, g, bn=(gamma, beta, mean, var), residual_in=rin, want_residual_out=True)
+        y = Wt.bn_apply(v, gamma, beta, mean, var, 1e-5).reshape(-1) + rin
+        assert np.array_equal(rout.view(np.uint64), y.view(np.uint64))
+        assert np.array_equal(Wt.unpack_act(bits2, P, Q, n, o).reshape(-1), (y >= 0))
+
+
+def test_error_classes_match_reference():  # test_bmm.cpp:156-174, test_bconv.cpp:330-361
+    a = md(4, 128, capi.ROW_PACKED)
+    A = np.zeros(8, np.uint64)
+    with pytest.raises(capi.BtnnError) as e:
+        B.bmm_pm1_bin(a, A, md(128, 4, capi.COL_PACKED), A, tau=np.zeros(3), kind=np.zeros(3))
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+    with pytest.raises(capi.BtnnError) as e:
+        B.bmm_pm1(md(4, 128, capi.FSB_ROW), np.zeros(16, np.uint64), md(128, 4, capi.COL_PACKED), A, capi.BMM_FSB)
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+    ad, g = capi.ActDesc(4, 4, 1, 16, 0, 8, 128), capi.ConvGeom(3, 3, 1, 1)
+    fd = capi.FilterDesc(3, 3, 8, 16, 0, 8, 128)
+    with pytest.raises(capi.BtnnError) as e:
+        B.bconv_fused(ad, np.zeros(64, np.uint64), fd, np.zeros(144, np.uint64), g, tau=np.zeros(8), kind=np.zeros(8),
+                      want_residual_out=True)
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+    with pytest.raises(capi.BtnnError) as e:
+        B.bconv_pm1(ad, np.zeros(64, np.uint64), capi.FilterDesc(3, 3, 8, 32, 0, 8, 128), np.zeros(144, np.uint64), g)
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+    with pytest.raises(capi.BtnnError) as e:
+        B.bconv_pm1(ad, np.zeros(64, np.uint64), fd, np.zeros(144, np.uint64), capi.ConvGeom(5, 5, 1, 1))
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+    with pytest.raises(capi.BtnnError) as e:
+        B.bconv_pm1(capi.ActDesc(2, 2, 1, 16, 0, 8, 128), np.zeros(16, np.uint64), fd, np.zeros(144, np.uint64),
+                    capi.ConvGeom(3, 3, 1, 0))
+    assert e.value.code == capi.BTNN_UNSUPPORTED_SHAPE

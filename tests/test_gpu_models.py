@@ -1,0 +1,89 @@
+"""GPU parity of the model driver (run_inference, inference.hpp:67-186): logits bit-exact
+(f64) and labels equal to the reference on the reference's own models and weights, in
+both weight layouts, and invariant to batch sharding across devices."""
+import numpy as np
+import pytest
+
+from fixtures import fixture_models
+from oracle_lib import oracle_run_inference
+from paper_2006_16578_b200 import btnn as B
+from paper_2006_16578_b200 import capi
+from paper_2006_16578_b200 import model as M
+from paper_2006_16578_b200 import weights as Wt
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("prefix,fm", fixture_models(), ids=lambda v: v if isinstance(v, str) else "")
+def test_run_inference_golden(prefix, fm):
+    plan = B.Plan(fm.spec, fm.store, fm.x.shape[0])
+    lg, lb = plan.run(fm.x)
+    assert np.array_equal(lg.view(np.uint64), fm.logits.view(np.uint64)), plan.engines()
+    assert np.array_equal(lb, fm.labels)
+    # the same plan again (graph replay) and a smaller batch reuse
+    lg2, _ = plan.run(fm.x)
+    assert np.array_equal(lg2.view(np.uint64), fm.logits.view(np.uint64))
+    if fm.x.shape[0] > 1:
+        lg3, lb3 = plan.run(fm.x[:1])
+        assert np.array_equal(lg3[0].view(np.uint64), fm.logits[0].view(np.uint64))
+
+
+@pytest.mark.parametrize("prefix,fm", fixture_models()[:6], ids=lambda v: v if isinstance(v, str) else "")
+def test_sharded_plan_matches(prefix, fm):
+    """Two shards on device 0 exercise the batch split; results equal the single run."""
+    plan = B.Plan(fm.spec, fm.store, fm.x.shape[0], devices=(0, 0))
+    lg, lb = plan.run(fm.x)
+    assert np.array_equal(lg.view(np.uint64), fm.logits.view(np.uint64))
+    assert np.array_equal(lb, fm.labels)
+
+
+def test_nonfinite_input_rejected():  # test_nn.cpp:355-364
+    m = M.make_model("bad", "4C3-8FC", 8, 8, 2, 3)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 67))
+    plan = B.Plan(m, ws, 2)
+    x = np.zeros((1, 8, 8, 2), np.float32)
+    x.reshape(-1)[7] = np.nan
+    with pytest.raises(capi.BtnnError) as e:
+        plan.run(x)
+    assert e.value.code == capi.BTNN_INVALID_INPUT
+    mm = M.make_model("mlp", "8FC", 4, 4, 1, 3)
+    p2 = B.Plan(mm, Wt.build_weights(mm, Wt.random_weights(mm, 3)), 2)
+    xb = np.ones((1, 4, 4, 1), np.float32)
+    xb[0, 1, 1, 0] = np.inf
+    with pytest.raises(capi.BtnnError):
+        p2.run(xb)
+
+
+@pytest.mark.parametrize("name,hw,batch", [("resnet18", 224, 2), ("alexnet", 224, 2), ("cifar-vgg", 32, 8),
+                                            ("mnist-mlp", 28, 64), ("cifar-resnet14", 32, 8), ("vgg16", 64, 2)])
+def test_stock_models_vs_oracle(name, hw, batch):
+    """The stock models (numpy-drawn weights) vs the C oracle; ResNet-18/AlexNet at full
+    ImageNet shape are checked on the small batch the bit-serial oracle affords."""
+    m = M.stock_model(name, hw, hw)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 1))
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((batch, m.in_h, m.in_w, m.in_c), dtype=np.float32)
+    plan = B.Plan(m, ws, batch)
+    lg, lb = plan.run(x)
+    if name in ("resnet18", "alexnet", "vgg16"):
+        ref = pytest.importorskip("oracle_lib").ref()
+        if ref is None:
+            pytest.skip("compiled reference not available")
+    want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x) if name not in ("resnet18", "alexnet", "vgg16") else \
+        _ref_run(m, ws, x)
+    assert np.array_equal(lg.view(np.uint64), want.view(np.uint64)), plan.engines()
+    assert np.array_equal(lb, wl)
+
+
+def _ref_run(m, ws, x):
+    """Large models: the reference's own run_inference (word-parallel, threaded) on the
+    same store, via oracle/_ref."""
+    import ctypes as C
+    from oracle_lib import ptr, ref
+    spec, store = m.c_spec(), ws.c_store()
+    lg = np.zeros(x.shape[0] * m.classes)
+    lb = np.zeros(x.shape[0], np.int32)
+    st = ref().ref_run_store(C.byref(spec), C.byref(store), ptr(np.ascontiguousarray(x), C.c_float), x.shape[0],
+                             ptr(lg, C.c_double), ptr(lb, C.c_int32))
+    assert st == 0, ref().ref_last_error()
+    return lg.reshape(x.shape[0], m.classes), lb
