@@ -81,7 +81,7 @@ class Clocks:
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and "Active" in s[2 + i]})
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons}
 
 
@@ -90,6 +90,80 @@ def peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def engine_peaks():
+    """Measured engine peaks on this B200 pool (profiles/microbench_r01.json)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "microbench_r01.json")))
+        return {"b1_mma_sync_tops": d["b1_mma_sync"]["t_bitops"], "tc_i8_tops": d["tc_i8_tmemA_n256"]["tops"],
+                "popc_tops": d["popc"]["t_bitops"], "dfma_tflops": d["dfma"]["tflops"]}
+    except Exception:
+        return {}
+
+
+def roofline(m, B, i, ms, engine):
+    """Roofline of layer i from its measured device time: algorithmic work per launch
+     / duration, against the measured peak of the bounding unit."""
+    L = m.layers[i]
+    hbm = peaks().get("hbm_gbs")
+    pk = engine_peaks()
+    sec = ms / 1e3
+    if L.kind == 0:  # f64 first layer: 2 flops per tap term
+        flops = 2.0 * L.out_h * L.out_w * B * L.in_channels * L.out_channels * L.kh * L.kw
+        a = flops / sec / 1e12
+        return {"bound": "fp64", "kernel": f"layer{i}:{engine}", "achieved": a, "peak": pk.get("dfma_tflops"),
+                "unit": "TFLOP/s", "frac": a / pk["dfma_tflops"] if pk else None, "traffic": None,
+                "peak_source": "profiles/microbench_r01.json dfma"}
+    if L.kind == 1 and (L.residual_in or L.residual_out):
+        # bn-route conv: the f64 taps dominate: 8 B per output written (+8 or 4x8 read)
+        outs = L.out_h * L.out_w * B * L.out_channels
+        rd = 0.0
+        if L.residual_in:
+            src = m.layers[L.shortcut_from]
+            rd = 8.0 * outs * (4 if src.out_h != L.out_h else 1) * min(src.out_channels, L.out_channels) / L.out_channels
+        byts = 8.0 * outs * (1 if L.residual_out else 0) + rd
+        a = byts / sec / 1e9
+        return {"bound": "hbm", "kernel": f"layer{i}:{engine}", "achieved": a, "peak": hbm, "unit": "GB/s",
+                "frac": a / hbm if hbm else None, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    if L.kind == 1:
+        ops = 2.0 * L.out_h * L.out_w * B * L.in_channels * L.out_channels * L.kh * L.kw
+    else:
+        ops = 2.0 * B * L.in_channels * L.units
+    a = ops / sec / 1e12
+    peak = pk.get("tc_i8_tops") if engine == "tc_i8" else pk.get("popc_tops")
+    return {"bound": "tensor" if engine == "tc_i8" else "int", "kernel": f"layer{i}:{engine}", "achieved": a,
+            "peak": peak, "unit": "TFLOP/s", "frac": a / peak if peak else None, "traffic": None,
+            "note": "bit-ops (1 MAC = 2 ops)", "peak_source": "profiles/microbench_r01.json"}
+
+
+def kernel_suites(reps=10, warmup=3):
+    """The reference's bmm / bmm-bin / bconv-bin suites (bench.hpp:129-299) at the BASELINE
+    points, device-timed through the C ABI: T bit-op/s and fractions of the measured b1
+    (emulated mma.sync) peak and of the engine's own (tcgen05 kind::i8) peak."""
+    import ctypes as C
+
+    from paper_2006_16578_b200 import capi
+
+    lib = capi.lib()
+    pk = engine_peaks()
+    out = {}
+    med, mn = C.c_double(), C.c_double()
+    eng = C.create_string_buffer(16)
+    for name, bin_ in (("bmm_1024", 0), ("bmm_bin_1024", 1)):
+        capi.check(lib.btnn_cuda_bench_bmm(1024, bin_, reps, warmup, C.byref(med), C.byref(mn), eng, 16))
+        tops = 2 * 1024 ** 3 / med.value / 1e3
+        out[name] = {"median_us": med.value / 1e3, "t_bitops": tops, "engine": eng.value.decode()}
+    # bconv-bin at the paper's Fig. sweep point C=O=512, 64x64, batch 16, K3 (bench.hpp:39-43)
+    for c in (128, 512, 2048):
+        capi.check(lib.btnn_cuda_bench_bconv(64, 16, c, c, 3, 1, reps, warmup, C.byref(med), C.byref(mn), eng, 16))
+        tops = 2 * 64 * 64 * 16 * c * c * 9 / med.value / 1e3
+        out[f"bconv_bin_c{c}"] = {"median_us": med.value / 1e3, "t_bitops": tops, "engine": eng.value.decode()}
+    for v in out.values():
+        if pk:
+            v["frac_of_b1_peak"] = v["t_bitops"] / pk["b1_mma_sync_tops"]
+            v["frac_of_tc_i8_peak"] = v["t_bitops"] / pk["tc_i8_tops"]
+    return out
 
 
 # ------------------------------------------------------------------ CPU reference arm
@@ -167,6 +241,7 @@ def main():
     import torch
 
     from paper_2006_16578_b200 import btnn
+    from paper_2006_16578_b200 import dist as D
     from paper_2006_16578_b200 import model as M
     from paper_2006_16578_b200 import weights as W
 
@@ -181,7 +256,8 @@ def main():
     x = torch.randn((B, m.in_h, m.in_w, m.in_c), device=dev, dtype=torch.float32, generator=gen)
     logits = torch.empty((B, m.classes), device=dev, dtype=torch.float64)
     labels = torch.empty((B,), device=dev, dtype=torch.int32)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)  # non-default: its handle orders the plan's graph
+    torch.cuda.set_stream(stream)
 
     def step():
         plan.run_device(x.data_ptr(), B, logits.data_ptr(), labels.data_ptr(), stream.cuda_stream)
@@ -203,9 +279,7 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     if dist:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = D.max_over_ranks(ms, dev)
     ms_per_step = ms / a.steps
     value = B * world * a.steps / (ms / 1e3)
     launches = plan.launches(B)
@@ -234,9 +308,7 @@ def main():
         e2e_step()
     e2e_s = time.perf_counter() - t0
     if dist:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = D.max_over_ranks(e2e_s, dev)
     e2e = B * world * a.steps / e2e_s
 
     # ---- per-layer device times (separate timed pass, per-layer CUDA events)
@@ -249,23 +321,8 @@ def main():
     layer_ms /= max(3, a.steps // 4)
     engines = plan.engines()
     top = int(np.argmax(layer_ms))
-    L = m.layers[top]
-    pk = peaks()
-    if L.kind in (1,) or L.kind in (3, 4):
-        # bit layer: algorithmic bit-ops = 2*P*Q*N*C*O*K^2 (bench.hpp:290-292) / 2*M*N*K
-        if L.kind == 1:
-            ops = 2.0 * L.out_h * L.out_w * B * L.in_channels * L.out_channels * L.kh * L.kw
-        else:
-            ops = 2.0 * B * L.in_channels * L.units
-        achieved = ops / (layer_ms[top] / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": f"layer{top}:{engines[top]}", "achieved": achieved,
-                "peak": None, "unit": "TFLOP/s", "frac": None, "traffic": None,
-                "note": "bit-ops (1 MAC = 2 ops); peak = measured engine peak (profiles/)"}
-    else:
-        flops = 2.0 * L.out_h * L.out_w * B * L.in_channels * L.out_channels * L.kh * L.kw
-        achieved = flops / (layer_ms[top] / 1e3) / 1e12
-        roof = {"bound": "fp64", "kernel": f"layer{top}:{engines[top]}", "achieved": achieved, "peak": None,
-                "unit": "TFLOP/s", "frac": None, "traffic": None, "note": "f64 first layer"}
+    roof = roofline(m, B, top, layer_ms[top], engines[top])
+    roof["share_of_step"] = float(layer_ms[top] / layer_ms.sum())
 
     out = None
     if rank == 0:
@@ -290,6 +347,10 @@ def main():
                "paper_turing_img_s": PAPER_IMG_S,
                "clocks": clk.summary(),
                "cpu_baseline": cpu}
+        try:
+            out["kernels"] = kernel_suites()
+        except Exception as ex:  # the model line stays valid even if a suite fails
+            out["kernels"] = {"error": str(ex)}
         print(json.dumps(out))
     if dist:
         dist.barrier()

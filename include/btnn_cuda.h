@@ -104,6 +104,12 @@ const char* btnn_cuda_last_error(void);
 int btnn_cuda_device_count(int* n);
 /* Device used by the kernel-level calls issued from this host thread (default 0). */
 int btnn_cuda_set_device(int device);
+/* Bit-GEMM engine for subsequent BMM/BConv launches (process-wide): 0 = auto (tcgen05
+ * kind::i8 tensor cores where the shape is covered, else CUDA-core LOP3+POPC),
+ * 1 = force LOP3+POPC, 2 = force tensor cores (fails with BTNN_UNSUPPORTED_SHAPE when
+ * a shape is not covered). Plans bind the engine when their graph is captured. */
+enum { BTNN_ENGINE_AUTO = 0, BTNN_ENGINE_POPC = 1, BTNN_ENGINE_TC = 2 };
+int btnn_cuda_set_engine(int engine);
 
 /* ---- storage sizes (words of uint64) --------------------------------------------- */
 size_t btnn_cuda_matrix_words(const btnn_matrix_desc* d);     /* BitMatrix::storage_bits/64 */
@@ -159,6 +165,19 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
 /* or_pool (bconv.hpp:247-272). */
 int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t window,
                       size_t stride, uint64_t* out_words);
+
+/* ---- benchmark suites (bench.hpp:129-299), device-timed ---------------------------- */
+/* bench_bmm: n x n x n; bin = 0 -> "bmm" (binarize float operands + bmm_pm1, int32 out),
+ * bin = 1 -> "bmm-bin" (packed operands, bmm_pm1_bin sign rule). Random device operands;
+ * median/min of `reps` CUDA-event-timed repetitions after `warmup`. `engine` receives the
+ * engine name. Throughput = 2n^3 / median (bench.hpp:207-209). */
+int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
+                        size_t engine_len);
+/* bench_bconv: input_hw x input_hw x batch x c -> o, k x k kernel, stride 1, pad k/2;
+ * bin = 0 -> "bconv" (binarize + bconv_pm1), bin = 1 -> "bconv-bin" (bconv_fused with sign
+ * thresholds, bench.hpp:238). Throughput = 2*P*Q*N*C*O*K^2 / median (bench.hpp:290-292). */
+int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
+                          double* median_ns, double* min_ns, char* engine, size_t engine_len);
 
 /* ---- model driver (inference.hpp:67-186) ----------------------------------------- */
 /* LayerSpec (model.hpp:36-52), already resolved (resolve_model, model.hpp:190-296). */
@@ -222,6 +241,10 @@ int btnn_cuda_plan_layer_ms(btnn_plan* plan, double* ms, size_t n_layers);
 int btnn_cuda_plan_set_breakdown(btnn_plan* plan, int enabled);
 /* Kernel launches per plan_run on one shard (for the bench's gpu_launches). */
 int btnn_cuda_plan_launches(btnn_plan* plan, size_t batch, size_t* launches);
+/* Inspection: copy the f64 residual tap (RealTensorPQNO, out_h*out_w*batch*out_channels
+ * doubles) that layer i wrote during the last run on shard 0. BTNN_INVALID_INPUT if the
+ * layer has no residual_out port. */
+int btnn_cuda_plan_read_tap(btnn_plan* plan, size_t i, size_t batch, double* out);
 /* Name of the engine chosen for layer i ("tc_i8", "popc", "fp64", "orpool", ...). */
 const char* btnn_cuda_plan_layer_engine(btnn_plan* plan, size_t i);
 int btnn_cuda_plan_destroy(btnn_plan* plan);

@@ -227,6 +227,13 @@ class Plan:
         check(lib().btnn_cuda_plan_launches(self.h, batch, C.byref(n)))
         return n.value
 
+    def read_tap(self, i: int, batch: int):
+        """The f64 residual tap layer i wrote in the last run (shard 0), PQNO flat."""
+        l = self.model.layers[i]
+        out = np.zeros(l.out_h * l.out_w * batch * l.out_channels, dtype=np.float64)
+        check(lib().btnn_cuda_plan_read_tap(self.h, i, batch, _p(out, C.c_double)))
+        return out
+
     def engines(self):
         return [lib().btnn_cuda_plan_layer_engine(self.h, i).decode() for i in range(self.n_layers)]
 

@@ -17,6 +17,7 @@ ROW_PACKED, COL_PACKED, FSB_ROW, FSB_COL = range(4)
 BMM_NAIVE, BMM_BLOCKED, BMM_FSB = range(3)
 GEQ, LEQ, CONST_PLUS, CONST_MINUS = range(4)
 FIRST_CONV_BWN, BIT_CONV, OR_POOL, BIT_FC, LAST_FC = range(5)
+ENGINE_AUTO, ENGINE_POPC, ENGINE_TC = range(3)
 
 sz = C.c_size_t
 
@@ -93,6 +94,7 @@ _PROTOS = {
     "btnn_cuda_last_error": (C.c_char_p, []),
     "btnn_cuda_device_count": (C.c_int, [P(C.c_int)]),
     "btnn_cuda_set_device": (C.c_int, [C.c_int]),
+    "btnn_cuda_set_engine": (C.c_int, [C.c_int]),
     "btnn_cuda_matrix_words": (sz, [P(MatrixDesc)]),
     "btnn_cuda_act_words": (sz, [P(ActDesc)]),
     "btnn_cuda_filter_words": (sz, [P(FilterDesc)]),
@@ -109,12 +111,15 @@ _PROTOS = {
     "btnn_cuda_bconv_fused": (C.c_int, [P(ActDesc), u64p, P(FilterDesc), u64p, P(ConvGeom), P(ConvFused), u64p]),
     "btnn_cuda_first_conv_bwn": (C.c_int, [f32p, sz, sz, sz, sz, f32p, sz, sz, sz, sz, P(ConvGeom), f64p]),
     "btnn_cuda_or_pool": (C.c_int, [P(ActDesc), u64p, sz, sz, u64p]),
+    "btnn_cuda_bench_bmm": (C.c_int, [sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz]),
+    "btnn_cuda_bench_bconv": (C.c_int, [sz, sz, sz, sz, sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz]),
     "btnn_cuda_plan_create": (C.c_int, [P(ModelSpec), P(WeightStore), sz, P(C.c_int), C.c_int, P(C.c_void_p)]),
     "btnn_cuda_plan_run": (C.c_int, [C.c_void_p, f32p, sz, f64p, i32p]),
     "btnn_cuda_plan_run_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, sz, C.c_void_p, C.c_void_p, C.c_void_p]),
     "btnn_cuda_plan_layer_ms": (C.c_int, [C.c_void_p, f64p, sz]),
     "btnn_cuda_plan_set_breakdown": (C.c_int, [C.c_void_p, C.c_int]),
     "btnn_cuda_plan_launches": (C.c_int, [C.c_void_p, sz, P(sz)]),
+    "btnn_cuda_plan_read_tap": (C.c_int, [C.c_void_p, sz, sz, f64p]),
     "btnn_cuda_plan_layer_engine": (C.c_char_p, [C.c_void_p, sz]),
     "btnn_cuda_plan_destroy": (C.c_int, [C.c_void_p]),
 }
@@ -139,3 +144,8 @@ def lib() -> C.CDLL:
 def check(status: int) -> None:
     if status != BTNN_OK:
         raise BtnnError(status, lib().btnn_cuda_last_error().decode())
+
+
+def set_engine(engine: int) -> None:
+    """btnn_cuda_set_engine: 0 auto, 1 LOP3+POPC, 2 tcgen05 tensor cores."""
+    check(lib().btnn_cuda_set_engine(engine))

@@ -45,6 +45,7 @@ void bn_to_device_arrays(const btnn_bn& bn, std::vector<double>& packed);
 // Engine selection for one implicit GEMM. Auto picks the tensor-core path when the shape
 // and epilogue are covered by it and an expanded filter is available, else LOP3+POPC.
 enum class EngineHint { Auto, Popc, TcI8 };
+int engine_override();  // btnn_cuda_set_engine
 
 // Tensor-core operand prepared once per filter (see kernels_tc.cu): +-1 int8 expansion
 // of the filter in the UMMA canonical layout, plus per-(tap, o) logical weight sums.

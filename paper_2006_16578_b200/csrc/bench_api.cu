@@ -1,0 +1,205 @@
+// bench_api.cu — device-timed versions of the reference benchmark suites
+// (bench.hpp:129-299): bmm / bmm-bin over n x n x n, bconv / bconv-bin over
+// input x input x batch x C -> O with a k x k kernel, stride 1, pad k/2.
+//
+//   bmm        float operands binarized on the device (pack_matrix) + bmm_pm1 (int32)
+//   bmm-bin    packed operands + bmm_pm1_bin with the sign rule (bit output)
+//   bconv      float input binarized (pack_nhwc) + bconv_pm1 (int32 PQNO)
+//   bconv-bin  packed input + bconv_fused with sign thresholds (tau = 0, Geq; bench.hpp:238)
+//
+// Operands are random on the device, timing is CUDA events around each launch sequence
+// after `warmup` untimed repetitions; median and min over `reps` (bench.hpp:51-70).
+// Throughput (reported by the caller) uses the reference's op counts: 2n^3 and
+// 2*P*Q*N*C*O*K^2 (bench.hpp:207-209, 290-292).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "api_internal.cuh"
+#include "layout.cuh"
+
+namespace btnn_gpu {
+
+__global__ void rand_words_kernel(uint64_t* w, size_t n, uint64_t seed) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + i * 0x9E3779B97F4A7C15ull;  // splitmix64
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    w[i] = z ^ (z >> 31);
+  }
+}
+__global__ void rand_floats_kernel(float* x, size_t n, uint64_t seed) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + i * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    x[i] = (float)((int64_t)(z ^ (z >> 31)) >> 40) * (1.0f / 8388608.0f);  // symmetric, zero-mean
+  }
+}
+static void rand_words(uint64_t* w, size_t n, uint64_t seed, cudaStream_t st) {
+  rand_words_kernel<<<148 * 8, 256, 0, st>>>(w, n, seed);
+  BT_CUDA(cudaGetLastError());
+}
+static void rand_floats(float* x, size_t n, uint64_t seed, cudaStream_t st) {
+  rand_floats_kernel<<<148 * 8, 256, 0, st>>>(x, n, seed);
+  BT_CUDA(cudaGetLastError());
+}
+
+template <class F>
+static void time_reps(int reps, int warmup, cudaStream_t st, F&& fn, double* median_ns, double* min_ns) {
+  require(reps >= 1, BTNN_INVALID_INPUT, "bench: need at least one repetition");
+  for (int i = 0; i < warmup; ++i) fn();
+  cudaEvent_t a, b;
+  BT_CUDA(cudaEventCreate(&a));
+  BT_CUDA(cudaEventCreate(&b));
+  std::vector<double> ns(reps);
+  for (int r = 0; r < reps; ++r) {
+    BT_CUDA(cudaEventRecord(a, st));
+    fn();
+    BT_CUDA(cudaEventRecord(b, st));
+    BT_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    BT_CUDA(cudaEventElapsedTime(&ms, a, b));
+    ns[r] = ms * 1e6;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  std::sort(ns.begin(), ns.end());
+  *median_ns = reps % 2 ? ns[reps / 2] : 0.5 * (ns[reps / 2 - 1] + ns[reps / 2]);
+  *min_ns = ns.front();
+}
+
+}  // namespace btnn_gpu
+
+using namespace btnn_gpu;
+
+extern "C" {
+
+int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
+                        size_t engine_len) {
+  return guard([&] {
+    require(n > 0, BTNN_INVALID_INPUT, "bench_bmm: zero size");
+    int dev = 0;
+    BT_CUDA(cudaGetDevice(&dev));
+    cudaStream_t st;
+    BT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const size_t kw = ru(n, 128) / 64;
+    DevBuf a(n * kw * 8), b(n * kw * 8), out_i(bin ? 0 : n * n * 4), out_b(bin ? n * kw * 8 : 0), fa, fb, flag(4);
+    ConvShape s{};
+    s.P = s.Q = s.H = s.W = 1;
+    s.KH = s.KW = s.stride = 1;
+    s.N = (int)n;
+    s.in_rps = s.out_rps = (int)n;
+    s.cw = (int)kw;
+    s.C = (int)n;
+    s.O = (int)n;
+    s.f_rps = (int)n;
+    s.cwo = (int)kw;
+    Epi e;
+    if (bin) {
+      rand_words(a.get<uint64_t>(), n * kw, 1, st);
+      rand_words(b.get<uint64_t>(), n * kw, 2, st);
+      e.mode = EPI_BITS;
+      e.out_bits = out_b.get<uint64_t>();
+    } else {
+      fa.alloc(n * n * 4);
+      fb.alloc(n * n * 4);
+      rand_floats(fa.get<float>(), n * n, 1, st);
+      rand_floats(fb.get<float>(), n * n, 2, st);  // B^T row-major: column j of B contiguous
+      e.mode = EPI_I32;
+      e.out_i32 = out_i.get<int32_t>();
+    }
+    TcFilter tcf;
+    if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
+    const char* used = "popc";
+    auto step = [&] {
+      if (!bin) {
+        launch_pack_rows(fa.get<float>(), n, n, kw * 2, a.get<uint32_t>(), flag.get<int>(), st);
+        launch_pack_rows(fb.get<float>(), n, n, kw * 2, b.get<uint32_t>(), flag.get<int>(), st);
+        if (tcf.valid()) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);  // re-expand the new B
+      }
+      used = launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
+    };
+    BT_CUDA(cudaStreamSynchronize(st));
+    time_reps(reps, warmup, st, step, median_ns, min_ns);
+    if (engine && engine_len) {
+      std::snprintf(engine, engine_len, "%s", used);
+    }
+    cudaStreamDestroy(st);
+  });
+}
+
+int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
+                          double* median_ns, double* min_ns, char* engine, size_t engine_len) {
+  return guard([&] {
+    require(input_hw && batch && c && o && k, BTNN_INVALID_INPUT, "bench_bconv: zero size");
+    cudaStream_t st;
+    BT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    const size_t H = input_hw, pad = k / 2;
+    const size_t P = (H + 2 * pad - k) + 1;
+    const size_t np = act_npad(batch, 0, 0), cp = act_cpad(c, 0, 0), op = act_cpad(o, 0, 0);
+    DevBuf in(H * H * np * cp / 8), filt(k * k * filt_opad(o, 0, 0) * cp / 8), x, flag(4);
+    DevBuf out_b(bin ? P * P * np * op / 8 : 0), out_i(bin ? 0 : P * P * batch * o * 4), lo, hi;
+    ConvShape s{};
+    s.P = s.Q = (int)P;
+    s.H = s.W = (int)H;
+    s.KH = s.KW = (int)k;
+    s.stride = 1;
+    s.pad = (int)pad;
+    s.N = (int)batch;
+    s.in_rps = s.out_rps = (int)np;
+    s.cw = (int)(cp / 64);
+    s.C = (int)c;
+    s.O = (int)o;
+    s.f_rps = (int)filt_opad(o, 0, 0);
+    s.cwo = (int)(op / 64);
+    // filter words: random, pad bits cleared by packing random floats per plane row
+    {
+      DevBuf fw(k * k * filt_opad(o, 0, 0) * c * 4);
+      rand_floats(fw.get<float>(), k * k * filt_opad(o, 0, 0) * c, 7, st);
+      BT_CUDA(cudaMemsetAsync(filt.get(), 0, filt.bytes(), st));
+      launch_pack_rows(fw.get<float>(), k * k * filt_opad(o, 0, 0), c, cp / 32, filt.get<uint32_t>(), flag.get<int>(), st);
+      BT_CUDA(cudaStreamSynchronize(st));
+    }
+    Epi e;
+    if (bin) {
+      BT_CUDA(cudaMemsetAsync(in.get(), 0, in.bytes(), st));
+      DevBuf fx(batch * H * H * c * 4);
+      rand_floats(fx.get<float>(), batch * H * H * c, 3, st);
+      launch_pack_nhwc(fx.get<float>(), (int)batch, (int)H, (int)H, (int)c, (int)np, (int)cp, in.get<uint32_t>(),
+                       flag.get<int>(), st);
+      BT_CUDA(cudaStreamSynchronize(st));
+      std::vector<long long> l(o, 0), h(o, 1LL << 40);  // sign rule: v >= 0 (tau = 0, Geq)
+      lo = upload(l.data(), o, st);
+      hi = upload(h.data(), o, st);
+      e.mode = EPI_BITS;
+      e.out_bits = out_b.get<uint64_t>();
+      e.thr_lo = lo.get<long long>();
+      e.thr_hi = hi.get<long long>();
+    } else {
+      x.alloc(batch * H * H * c * 4);
+      rand_floats(x.get<float>(), batch * H * H * c, 3, st);
+      e.mode = EPI_I32;
+      e.out_i32 = out_i.get<int32_t>();
+    }
+    TcFilter tcf;
+    if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, filt.get<uint64_t>(), tcf, st);
+    const char* used = "popc";
+    auto step = [&] {
+      if (!bin) {
+        BT_CUDA(cudaMemsetAsync(in.get(), 0, in.bytes(), st));
+        launch_pack_nhwc(x.get<float>(), (int)batch, (int)H, (int)H, (int)c, (int)np, (int)cp, in.get<uint32_t>(),
+                         flag.get<int>(), st);
+      }
+      used = launch_bgemm(s, in.get<uint64_t>(), filt.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
+    };
+    BT_CUDA(cudaStreamSynchronize(st));
+    time_reps(reps, warmup, st, step, median_ns, min_ns);
+    if (engine && engine_len) std::snprintf(engine, engine_len, "%s", used);
+    cudaStreamDestroy(st);
+  });
+}
+
+}  // extern "C"

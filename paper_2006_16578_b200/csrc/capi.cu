@@ -173,6 +173,17 @@ static BmmOperands stage_bmm(const btnn_matrix_desc* a, const uint64_t* aw, cons
 
 static void use_device() { BT_CUDA(cudaSetDevice(g_device)); }
 
+// One implicit GEMM for a kernel-level call: the tensor-core operand is expanded from
+// the caller's filter for this call (a plan does it once at creation).
+static const char* run_gemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e,
+                            cudaStream_t st) {
+  TcFilter tcf;
+  if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, filt, tcf, st);
+  const char* engine = launch_bgemm(s, act, filt, e, st, EngineHint::Auto, &tcf);
+  BT_CUDA(cudaStreamSynchronize(st));  // tcf is released at scope exit
+  return engine;
+}
+
 }  // namespace btnn_gpu
 
 using namespace btnn_gpu;
@@ -382,7 +393,7 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
       e.mode = EPI_I32;
       e.raw = which == 0;
       e.out_i32 = o.get<int32_t>();
-      launch_bgemm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st, EngineHint::Auto);
+      run_gemm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st);
       BT_CUDA(cudaMemcpy(out, o.get(), a->rows * b->cols * 4, cudaMemcpyDeviceToHost));
       return;
     }
@@ -398,7 +409,7 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
     BT_CUDA(cudaMemsetAsync(rp.get(), 0, rp.bytes(), st));
     e.mode = EPI_BITS;
     e.out_bits = rp.get<uint64_t>();
-    launch_bgemm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st, EngineHint::Auto);
+    run_gemm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st);
     const int out_layout = a->layout == BTNN_FSB_ROW ? BTNN_FSB_ROW : BTNN_ROW_PACKED;
     const size_t words = mat_words(a->rows, b->cols, out_layout, a->bh, a->bw);
     if (out_layout == BTNN_ROW_PACKED) {
@@ -492,7 +503,7 @@ int btnn_cuda_bconv_pm1(const btnn_act_desc* in, const uint64_t* iw, const btnn_
     Epi e;
     e.mode = EPI_I32;
     e.out_i32 = o.get<int32_t>();
-    launch_bgemm(op.s, op.in.get<uint64_t>(), op.filt.get<uint64_t>(), e, st, EngineHint::Auto);
+    run_gemm(op.s, op.in.get<uint64_t>(), op.filt.get<uint64_t>(), e, st);
     BT_CUDA(cudaMemcpy(out, o.get(), n_out * 4, cudaMemcpyDeviceToHost));
   });
 }
@@ -549,7 +560,7 @@ int btnn_cuda_bconv_fused(const btnn_act_desc* in, const uint64_t* iw, const btn
     DevBuf ob(plain_words * 8);
     BT_CUDA(cudaMemsetAsync(ob.get(), 0, ob.bytes(), st));
     e.out_bits = ob.get<uint64_t>();
-    launch_bgemm(op.s, op.in.get<uint64_t>(), op.filt.get<uint64_t>(), e, st, EngineHint::Auto);
+    run_gemm(op.s, op.in.get<uint64_t>(), op.filt.get<uint64_t>(), e, st);
     if (fu->residual_out) BT_CUDA(cudaMemcpyAsync(fu->residual_out, drout.get(), n_out * 8, cudaMemcpyDeviceToHost, st));
     if (!in->tiled) {
       BT_CUDA(cudaMemcpyAsync(out, ob.get(), plain_words * 8, cudaMemcpyDeviceToHost, st));
@@ -587,6 +598,10 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
     a.N = (int)batch; a.H = (int)height; a.W = (int)width; a.C = (int)channels; a.O = (int)out_channels;
     a.KH = (int)kh; a.KW = (int)kw; a.stride = (int)g->stride; a.pad = (int)g->pad; a.P = (int)P; a.Q = (int)Q;
     a.out_acc = o.get<double>();
+    const int K = (int)(kh * kw * channels);
+    DevBuf wb(first_conv_signbits_words((int)out_channels, K) * 4);
+    launch_first_conv_signbits(dw.get<float>(), (int)out_channels, K, wb.get<uint32_t>(), st);
+    a.wbits = wb.get<uint32_t>();
     launch_first_conv(a, st);
     BT_CUDA(cudaMemcpy(out, o.get(), n_out * 8, cudaMemcpyDeviceToHost));
   });

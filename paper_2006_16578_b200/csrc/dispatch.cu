@@ -1,10 +1,31 @@
 // dispatch.cu — engine selection for the implicit bit GEMM.
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+
 #include "api_internal.cuh"
+
+#include <atomic>
 
 namespace btnn_gpu {
 
+// Initial engine from BTNN_ENGINE=auto|popc|tc (btnn_cuda_set_engine overrides it).
+static int engine_from_env() {
+  const char* v = std::getenv("BTNN_ENGINE");
+  if (v && !std::strcmp(v, "popc")) return BTNN_ENGINE_POPC;
+  if (v && !std::strcmp(v, "tc")) return BTNN_ENGINE_TC;
+  return BTNN_ENGINE_AUTO;
+}
+static std::atomic<int> g_engine{engine_from_env()};
+
+int engine_override() { return g_engine.load(); }
+
 const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e, cudaStream_t st,
                          EngineHint h, const TcFilter* tc) {
+  if (h == EngineHint::Auto) {
+    const int o = g_engine.load();
+    h = o == BTNN_ENGINE_POPC ? EngineHint::Popc : o == BTNN_ENGINE_TC ? EngineHint::TcI8 : EngineHint::Auto;
+  }
   const bool tc_ok = tc && tc->valid() && tc_supported(s, e);
   if (h == EngineHint::TcI8) require(tc_ok, BTNN_UNSUPPORTED_SHAPE, "tensor-core engine does not cover this shape");
   if (tc_ok && h != EngineHint::Popc) {
@@ -16,3 +37,11 @@ const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t
 }
 
 }  // namespace btnn_gpu
+
+extern "C" int btnn_cuda_set_engine(int engine) {
+  return btnn_gpu::guard([&] {
+    btnn_gpu::require(engine >= BTNN_ENGINE_AUTO && engine <= BTNN_ENGINE_TC, BTNN_INVALID_INPUT,
+                      "set_engine: unknown engine");
+    btnn_gpu::g_engine.store(engine);
+  });
+}

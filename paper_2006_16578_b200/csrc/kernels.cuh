@@ -58,8 +58,11 @@ struct FirstConvArgs {
   double* tap;            // optional, PQNO
   uint64_t* out_bits;     // optional, HWNC plain (pre-zeroed)
   int out_rps, cwo;
+  const uint32_t* wbits = nullptr;  // optional per-o sign bits (launch_first_conv_signbits)
 };
 void launch_first_conv(const FirstConvArgs& a, cudaStream_t st);
+size_t first_conv_signbits_words(int O, int K);
+void launch_first_conv_signbits(const float* w_pm1, int O, int K, uint32_t* out, cudaStream_t st);
 
 // Format stage.
 void launch_check_finite(const float* x, size_t n, int* flag, cudaStream_t st);

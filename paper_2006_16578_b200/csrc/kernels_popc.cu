@@ -240,9 +240,128 @@ __global__ void first_conv_kernel(FirstConvArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------------------
+// First layer, register-blocked variant for the stock shapes (KHxKWxC compile-time,
+// O % 32 == 0, O <= 128). One block per (image n, output row p); warp w owns sites
+// q = 8w..8w+7 of that row, lane l owns channels o = l + 32j (j < J). The KH input rows
+// are staged in shared memory as f64 (zero outside the frame: adding +-0.0 to an
+// accumulator that starts at +0.0 leaves it unchanged, so zero-fill is bit-identical to
+// the reference's skip). Each term is DFMA(x, +-1.0, acc): x * (+-1) is exact, so the
+// single rounding equals the reference's add (bconv.hpp:233-234), in the same
+// (r, s, c) order. Weight signs live in registers (one bit per (o, k)).
+// ------------------------------------------------------------------------------------
+template <int KH, int KW, int C, int J>
+__global__ void __launch_bounds__(256) first_conv_tiled_kernel(FirstConvArgs a, const uint32_t* __restrict__ wbits) {
+  constexpr int K = KH * KW * C, KWORDS = (K + 31) / 32, SQ = 8;
+  extern __shared__ double patch[];  // [KH][Wp][C], Wp = W + 2*pad + slack
+  const int n = blockIdx.x / a.P, p = blockIdx.x % a.P;
+  const int Wp = (a.Q - 1) * a.stride + KW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // stage rows hh = p*stride - pad + r, cols ww = col - pad
+  for (int i = threadIdx.x; i < KH * Wp * C; i += blockDim.x) {
+    const int c = i % C, col = (i / C) % Wp, r = i / (C * Wp);
+    const int hh = p * a.stride - a.pad + r, ww = col - a.pad;
+    double v = 0.0;
+    if (hh >= 0 && hh < a.H && ww >= 0 && ww < a.W) v = (double)__ldg(a.x + (((size_t)n * a.H + hh) * a.W + ww) * C + c);
+    patch[i] = v;
+  }
+  uint32_t wb[J][KWORDS];
+#pragma unroll
+  for (int j = 0; j < J; ++j)
+#pragma unroll
+    for (int w = 0; w < KWORDS; ++w) wb[j][w] = __ldg(wbits + (size_t)(lane + 32 * j) * KWORDS + w);
+  __syncthreads();
+  const int q0 = warp * SQ;
+  if (q0 >= a.Q) return;  // whole warp idle (no ballots pending)
+  double acc[SQ][J];
+#pragma unroll
+  for (int i = 0; i < SQ; ++i)
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[i][j] = 0.0;
+#pragma unroll
+  for (int r = 0; r < KH; ++r)
+#pragma unroll
+    for (int s = 0; s < KW; ++s)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        constexpr int dummy = 0;
+        (void)dummy;
+        const int k = (r * KW + s) * C + c;
+        double w[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          w[j] = __hiloint2double((int)(0x3FF00000u | ((~wb[j][k >> 5] >> (k & 31)) & 1u) << 31), 0);
+        const double* base = patch + ((size_t)r * Wp + s) * C + c;
+#pragma unroll
+        for (int i = 0; i < SQ; ++i) {
+          const int q = min(q0 + i, a.Q - 1);
+          const double x = base[(size_t)q * a.stride * C];
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc[i][j] = __fma_rn(x, w[j], acc[i][j]);
+        }
+      }
+  uint32_t* ob = reinterpret_cast<uint32_t*>(a.out_bits);
+#pragma unroll
+  for (int i = 0; i < SQ; ++i) {
+    const int q = q0 + i;
+    const bool live = q < a.Q;
+    const int site = p * a.Q + (live ? q : 0);
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int o = lane + 32 * j;
+      const size_t idx = ((size_t)site * a.N + n) * a.O + o;
+      if (live && a.out_acc) a.out_acc[idx] = acc[i][j];
+      if (a.out_bits) {
+        const double y = bn_eval(acc[i][j], a.bn_mean[o], a.bn_s[o], a.bn_gamma[o], a.bn_beta[o]);
+        if (live && a.tap) a.tap[idx] = y;
+        const uint32_t bal = __ballot_sync(0xffffffffu, y >= 0.0);
+        if (live && lane == 0) ob[(((size_t)site * a.out_rps + n) * a.cwo * 64 + 32 * j) / 32] = bal;
+      }
+    }
+  }
+}
+
+// (o, r, s, c) +-1 floats -> per-o sign bits, bit k = (w >= 0) in (r, s, c) order.
+__global__ void first_conv_signbits_kernel(const float* __restrict__ w, int O, int K, int kwords, uint32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= O * kwords) return;
+  const int o = i / kwords, wd = i % kwords;
+  uint32_t v = 0;
+  for (int b = 0; b < 32; ++b) {
+    const int k = wd * 32 + b;
+    if (k < K && w[(size_t)o * K + k] >= 0.0f) v |= 1u << b;
+  }
+  out[i] = v;
+}
+
+size_t first_conv_signbits_words(int O, int K) { return (size_t)O * ((K + 31) / 32); }
+void launch_first_conv_signbits(const float* w_pm1, int O, int K, uint32_t* out, cudaStream_t st) {
+  const int kwords = (K + 31) / 32;
+  first_conv_signbits_kernel<<<(O * kwords + 127) / 128, 128, 0, st>>>(w_pm1, O, K, kwords, out);
+  BT_CUDA(cudaGetLastError());
+}
+
+template <int KH, int KW, int C, int J>
+static bool try_first_conv_tiled(const FirstConvArgs& a, cudaStream_t st) {
+  if (!a.wbits || a.KH != KH || a.KW != KW || a.C != C || a.O != 32 * J) return false;
+  const int Wp = (a.Q - 1) * a.stride + KW;
+  const size_t smem = (size_t)KH * Wp * C * sizeof(double);
+  const int warps = (a.Q + 7) / 8;
+  if (smem > 200 * 1024 || warps > 8) return false;
+  auto kern = first_conv_tiled_kernel<KH, KW, C, J>;
+  BT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)(a.N * a.P), 32 * warps, smem, st>>>(a, a.wbits);
+  BT_CUDA(cudaGetLastError());
+  return true;
+}
+
 void launch_first_conv(const FirstConvArgs& a, cudaStream_t st) {
   const size_t total = (size_t)a.P * a.Q * a.N * a.O;
   if (!total) return;
+  if (try_first_conv_tiled<7, 7, 3, 2>(a, st) || try_first_conv_tiled<11, 11, 3, 4>(a, st) ||
+      try_first_conv_tiled<3, 3, 3, 4>(a, st) || try_first_conv_tiled<3, 3, 3, 2>(a, st) ||
+      try_first_conv_tiled<7, 7, 3, 4>(a, st))
+    return;
   const int threads = 256;
   const size_t blocks = (total + threads - 1) / threads;
   first_conv_kernel<<<(unsigned)(blocks < 148 * 64 ? blocks : 148 * 64), threads, 0, st>>>(a);

@@ -29,6 +29,7 @@ struct LayerDev {
   DevBuf filt;          // plain KKOC filter / ColPacked fc matrix
   TcFilter tc;          // tensor-core operand (bit conv / fc when covered)
   DevBuf wpm1;          // first conv (o,r,s,c) floats
+  DevBuf wbits;         // first conv per-o sign bits
   DevBuf thr_lo, thr_hi;
   DevBuf bn;            // mean | s | gamma | beta
   bool has_thr = false, has_bn = false;
@@ -160,6 +161,9 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
     }
     if (l.kind == BTNN_FIRST_CONV_BWN) {
       L.wpm1 = upload(w.conv_pm1, w.conv_pm1_n, st);
+      const int K = (int)(l.kh * l.kw * l.in_channels);
+      L.wbits.alloc(first_conv_signbits_words((int)l.out_channels, K) * 4);
+      launch_first_conv_signbits(L.wpm1.get<float>(), (int)l.out_channels, K, L.wbits.get<uint32_t>(), st);
     } else if (l.kind == BTNN_BIT_CONV) {
       DevBuf raw = upload(w.filter_words, w.filter_n_words, st);
       if (!ws->tiled) {
@@ -244,6 +248,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       a.bn_mean = L.bn.get<double>(); a.bn_s = a.bn_mean + C4; a.bn_gamma = a.bn_mean + 2 * C4; a.bn_beta = a.bn_mean + 3 * C4;
       a.tap = l.residual_out ? L.tap.get<double>() : nullptr;
       a.out_bits = out;
+      a.wbits = L.wbits.get<uint32_t>();
       a.out_rps = (int)np;
       a.cwo = (int)(act_cpad(l.out_channels, 0, 0) / 64);
       launch_first_conv(a, st);
@@ -330,9 +335,11 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
   return launches;
 }
 
-// Enqueue via a cached CUDA graph (or eagerly when timing layers).
+// Enqueue via a cached CUDA graph (or eagerly when timing layers). The graph is
+// captured on the shard's stream and launched on `launch_stream` (the caller's stream
+// for run_device, the shard's own stream otherwise).
 static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_t batch, double* d_logits,
-                             int32_t* d_labels, bool timed) {
+                             int32_t* d_labels, bool timed, cudaStream_t launch_stream = nullptr) {
   if (timed) {
     sh.launches = enqueue_forward(plan, sh, d_x, batch, d_logits, d_labels, true);
     return;
@@ -356,7 +363,7 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
     sh.launches = n;
     it = sh.graphs.emplace(key, ex).first;
   }
-  BT_CUDA(cudaGraphLaunch(it->second, sh.stream));
+  BT_CUDA(cudaGraphLaunch(it->second, launch_stream ? launch_stream : sh.stream));
 }
 
 static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t batch, double* logits, int32_t* labels) {
@@ -466,20 +473,10 @@ int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size
     Shard& sh = *plan->shards[shard];
     require(batch > 0 && batch <= sh.max_batch, BTNN_INVALID_INPUT, "plan_run_device: batch out of range");
     BT_CUDA(cudaSetDevice(sh.device));
-    cudaStream_t user = static_cast<cudaStream_t>(stream);
-    cudaEvent_t ev;
-    if (user) {  // order the plan stream after the caller's stream
-      BT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      BT_CUDA(cudaEventRecord(ev, user));
-      BT_CUDA(cudaStreamWaitEvent(sh.stream, ev, 0));
-    }
+    // stream == NULL: the plan's own stream (caller synchronizes via the device);
+    // otherwise the graph is launched straight onto the caller's stream.
     run_shard_device(plan, sh, d_x, batch, d_logits ? d_logits : sh.logits.get<double>(),
-                     d_labels ? d_labels : sh.labels.get<int32_t>(), false);
-    if (user) {
-      BT_CUDA(cudaEventRecord(ev, sh.stream));
-      BT_CUDA(cudaStreamWaitEvent(user, ev, 0));
-      BT_CUDA(cudaEventDestroy(ev));
-    }
+                     d_labels ? d_labels : sh.labels.get<int32_t>(), false, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -502,6 +499,20 @@ int btnn_cuda_plan_launches(btnn_plan* plan, size_t batch, size_t* launches) {
     require(plan != nullptr, BTNN_INVALID_INPUT, "null plan");
     (void)batch;
     *launches = plan->shards[0]->launches;
+  });
+}
+
+int btnn_cuda_plan_read_tap(btnn_plan* plan, size_t i, size_t batch, double* out) {
+  return guard([&] {
+    require(plan && !plan->shards.empty() && i < plan->specs.size(), BTNN_INVALID_INPUT, "plan_read_tap: bad layer");
+    Shard& sh = *plan->shards[0];
+    const LayerDev& L = sh.layers[i];
+    require(L.spec.residual_out && L.tap.get(), BTNN_INVALID_INPUT, "plan_read_tap: layer has no residual_out");
+    require(batch > 0 && batch <= sh.max_batch, BTNN_INVALID_INPUT, "plan_read_tap: bad batch");
+    BT_CUDA(cudaSetDevice(sh.device));
+    BT_CUDA(cudaStreamSynchronize(sh.stream));
+    BT_CUDA(cudaMemcpy(out, L.tap.get(), L.spec.out_h * L.spec.out_w * batch * L.spec.out_channels * sizeof(double),
+                       cudaMemcpyDeviceToHost));
   });
 }
 

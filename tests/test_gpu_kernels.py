@@ -12,7 +12,7 @@ from paper_2006_16578_b200 import btnn as B
 from paper_2006_16578_b200 import capi
 from paper_2006_16578_b200 import weights as Wt
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("engine")]
 
 
 def md(r, c, lay, bh=8, bw=128):

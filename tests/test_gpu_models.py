@@ -11,7 +11,7 @@ from paper_2006_16578_b200 import capi
 from paper_2006_16578_b200 import model as M
 from paper_2006_16578_b200 import weights as Wt
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("engine")]
 
 
 @pytest.mark.parametrize("prefix,fm", fixture_models(), ids=lambda v: v if isinstance(v, str) else "")
@@ -52,6 +52,22 @@ def test_nonfinite_input_rejected():  # test_nn.cpp:355-364
     xb[0, 1, 1, 0] = np.inf
     with pytest.raises(capi.BtnnError):
         p2.run(xb)
+
+
+@pytest.mark.parametrize("tokens,hw,shortcuts", [
+    # type-A shortcuts whose zero-filled channels end inside an output tile
+    ("8C3-24C3-40C3/2-40C3-72C3/2-72C3-8FC", 16, [(1, 3), (3, 5)]),
+    ("16C3-200C3-200C3/2-300C3-300C3", 12, [(1, 3), (3, 4)]),
+    ("32C3-64C3-128C3/2-256C3-256C3/2-256C3", 16, [(1, 3), (3, 5)]),
+])
+def test_residual_variants_vs_oracle(tokens, hw, shortcuts):
+    m = M.make_model("resvar", tokens, hw, hw, 3, 7, shortcuts)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 17))
+    x = np.random.default_rng(18).standard_normal((5, hw, hw, 3), dtype=np.float32)
+    lg, lb = B.Plan(m, ws, 5).run(x)
+    want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+    assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(lb, wl)
 
 
 @pytest.mark.parametrize("name,hw,batch", [("resnet18", 224, 2), ("alexnet", 224, 2), ("cifar-vgg", 32, 8),
