@@ -253,16 +253,18 @@ __global__ void first_conv_kernel(FirstConvArgs a) {
 template <int KH, int KW, int C, int J>
 __global__ void __launch_bounds__(256) first_conv_tiled_kernel(FirstConvArgs a, const uint32_t* __restrict__ wbits) {
   constexpr int K = KH * KW * C, KWORDS = (K + 31) / 32, SQ = 8;
-  extern __shared__ double patch[];  // [KH][Wp][C], Wp = W + 2*pad + slack
+  constexpr int CP = C == 3 ? 4 : C;  // channel pitch in smem: 3 -> 4 so a tap is one 16 B + one 8 B load
+  extern __shared__ double patch[];   // [KH][Wp][CP], Wp = W + 2*pad + slack
   const int n = blockIdx.x / a.P, p = blockIdx.x % a.P;
   const int Wp = (a.Q - 1) * a.stride + KW;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // stage rows hh = p*stride - pad + r, cols ww = col - pad
-  for (int i = threadIdx.x; i < KH * Wp * C; i += blockDim.x) {
-    const int c = i % C, col = (i / C) % Wp, r = i / (C * Wp);
+  for (int i = threadIdx.x; i < KH * Wp * CP; i += blockDim.x) {
+    const int c = i % CP, col = (i / CP) % Wp, r = i / (CP * Wp);
     const int hh = p * a.stride - a.pad + r, ww = col - a.pad;
     double v = 0.0;
-    if (hh >= 0 && hh < a.H && ww >= 0 && ww < a.W) v = (double)__ldg(a.x + (((size_t)n * a.H + hh) * a.W + ww) * C + c);
+    if (c < C && hh >= 0 && hh < a.H && ww >= 0 && ww < a.W)
+      v = (double)__ldg(a.x + (((size_t)n * a.H + hh) * a.W + ww) * C + c);
     patch[i] = v;
   }
   uint32_t wb[J][KWORDS];
@@ -278,28 +280,42 @@ __global__ void __launch_bounds__(256) first_conv_tiled_kernel(FirstConvArgs a, 
   for (int i = 0; i < SQ; ++i)
 #pragma unroll
     for (int j = 0; j < J; ++j) acc[i][j] = 0.0;
+  int qoff[SQ];  // smem offset of each site's window column
+#pragma unroll
+  for (int i = 0; i < SQ; ++i) qoff[i] = min(q0 + i, a.Q - 1) * a.stride * CP;
 #pragma unroll
   for (int r = 0; r < KH; ++r)
 #pragma unroll
-    for (int s = 0; s < KW; ++s)
+    for (int s = 0; s < KW; ++s) {
+      // this tap's +-1 weights once, then per site its C inputs (broadcast loads) and the
+      // terms in c order — every accumulator still sees (r, s, c) order.
+      double w[C][J];
 #pragma unroll
-      for (int c = 0; c < C; ++c) {
-        constexpr int dummy = 0;
-        (void)dummy;
-        const int k = (r * KW + s) * C + c;
-        double w[J];
+      for (int c = 0; c < C; ++c)
 #pragma unroll
-        for (int j = 0; j < J; ++j)
-          w[j] = __hiloint2double((int)(0x3FF00000u | ((~wb[j][k >> 5] >> (k & 31)) & 1u) << 31), 0);
-        const double* base = patch + ((size_t)r * Wp + s) * C + c;
-#pragma unroll
-        for (int i = 0; i < SQ; ++i) {
-          const int q = min(q0 + i, a.Q - 1);
-          const double x = base[(size_t)q * a.stride * C];
-#pragma unroll
-          for (int j = 0; j < J; ++j) acc[i][j] = __fma_rn(x, w[j], acc[i][j]);
+        for (int j = 0; j < J; ++j) {
+          const int k = (r * KW + s) * C + c;
+          w[c][j] = __hiloint2double((int)(0x3FF00000u | ((~wb[j][k >> 5] >> (k & 31)) & 1u) << 31), 0);
         }
+      const double* base = patch + ((size_t)r * Wp + s) * CP;
+#pragma unroll
+      for (int i = 0; i < SQ; ++i) {
+        double x[CP];
+        if constexpr (CP == 4) {
+          const double2 v01 = *reinterpret_cast<const double2*>(base + qoff[i]);
+          x[0] = v01.x;
+          x[1] = v01.y;
+          x[2] = base[qoff[i] + 2];
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; ++c) x[c] = base[qoff[i] + c];
+        }
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+#pragma unroll
+          for (int j = 0; j < J; ++j) acc[i][j] = __fma_rn(x[c], w[c][j], acc[i][j]);
       }
+    }
   uint32_t* ob = reinterpret_cast<uint32_t*>(a.out_bits);
 #pragma unroll
   for (int i = 0; i < SQ; ++i) {
@@ -345,7 +361,7 @@ template <int KH, int KW, int C, int J>
 static bool try_first_conv_tiled(const FirstConvArgs& a, cudaStream_t st) {
   if (!a.wbits || a.KH != KH || a.KW != KW || a.C != C || a.O != 32 * J) return false;
   const int Wp = (a.Q - 1) * a.stride + KW;
-  const size_t smem = (size_t)KH * Wp * C * sizeof(double);
+  const size_t smem = (size_t)KH * Wp * (C == 3 ? 4 : C) * sizeof(double);
   const int warps = (a.Q + 7) / 8;
   if (smem > 200 * 1024 || warps > 8) return false;
   auto kern = first_conv_tiled_kernel<KH, KW, C, J>;
