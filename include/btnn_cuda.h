@@ -166,6 +166,10 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
 int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t window,
                       size_t stride, uint64_t* out_words);
 
+/* Self-test of the bn-route division (csrc/bnmath.cuh): fast[i] = a[i]/b[i] through the
+ * per-channel-reciprocal path, ref[i] = __ddiv_rn(a[i], b[i]); host buffers of n doubles. */
+int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* fast, double* ref);
+
 /* ---- benchmark suites (bench.hpp:129-299), device-timed ---------------------------- */
 /* bench_bmm: n x n x n; bin = 0 -> "bmm" (binarize float operands + bmm_pm1, int32 out),
  * bin = 1 -> "bmm-bin" (packed operands, bmm_pm1_bin sign rule). Random device operands;
@@ -241,10 +245,15 @@ int btnn_cuda_plan_layer_ms(btnn_plan* plan, double* ms, size_t n_layers);
 int btnn_cuda_plan_set_breakdown(btnn_plan* plan, int enabled);
 /* Kernel launches per plan_run on one shard (for the bench's gpu_launches). */
 int btnn_cuda_plan_launches(btnn_plan* plan, size_t batch, size_t* launches);
-/* Inspection: copy the f64 residual tap (RealTensorPQNO, out_h*out_w*batch*out_channels
- * doubles) that layer i wrote during the last run on shard 0. BTNN_INVALID_INPUT if the
- * layer has no residual_out port. */
+/* Inspection: copy the f64 residual tap (RealTensorPQNO) that layer i stored during the
+ * last run on shard 0, dims[0]*dims[1]*batch*dims[3] doubles with dims from
+ * btnn_cuda_plan_tap_dims. BTNN_INVALID_INPUT if the layer has no residual_out port. */
 int btnn_cuda_plan_read_tap(btnn_plan* plan, size_t i, size_t batch, double* out);
+/* Shape of the stored tap of layer i: dims = {h, w, averaged, channels}. A layer whose
+ * only consumer halves the shortcut (adapt_shortcut, inference.hpp:43-63) stores the
+ * 2x2-averaged tap directly (averaged = 1, h = out_h/2, w = out_w/2); otherwise the full
+ * tap (averaged = 0). */
+int btnn_cuda_plan_tap_dims(btnn_plan* plan, size_t i, size_t* dims);
 /* Name of the engine chosen for layer i ("tc_i8", "popc", "fp64", "orpool", ...). */
 const char* btnn_cuda_plan_layer_engine(btnn_plan* plan, size_t i);
 int btnn_cuda_plan_destroy(btnn_plan* plan);

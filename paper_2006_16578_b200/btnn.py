@@ -227,10 +227,17 @@ class Plan:
         check(lib().btnn_cuda_plan_launches(self.h, batch, C.byref(n)))
         return n.value
 
+    def tap_dims(self, i: int):
+        """(h, w, averaged, channels) of the tap layer i stored in the last run."""
+        d = (C.c_size_t * 4)()
+        check(lib().btnn_cuda_plan_tap_dims(self.h, i, d))
+        return tuple(int(v) for v in d)
+
     def read_tap(self, i: int, batch: int):
-        """The f64 residual tap layer i wrote in the last run (shard 0), PQNO flat."""
-        l = self.model.layers[i]
-        out = np.zeros(l.out_h * l.out_w * batch * l.out_channels, dtype=np.float64)
+        """The f64 residual tap layer i stored in the last run (shard 0), PQNO flat: the
+        full tap, or the 2x2-averaged one when tap_dims(i)[2] == 1."""
+        h, w, _, c = self.tap_dims(i)
+        out = np.zeros(h * w * batch * c, dtype=np.float64)
         check(lib().btnn_cuda_plan_read_tap(self.h, i, batch, _p(out, C.c_double)))
         return out
 

@@ -41,6 +41,10 @@ size_t conv_out(size_t x, size_t k, size_t stride, size_t pad, bool height);
 void thresholds_to_int(const double* tau, const uint8_t* kind, size_t n, std::vector<long long>& lo,
                        std::vector<long long>& hi);
 void bn_to_device_arrays(const btnn_bn& bn, std::vector<double>& packed);
+// Uploads the bn block (bnmath.cuh: mean | s | gamma | beta | reciprocal) and fills the
+// reciprocal array on the device.
+DevBuf upload_bn(const btnn_bn& bn, cudaStream_t st);
+void launch_bn_recip(double* bn, int channels, cudaStream_t st);
 
 // Engine selection for one implicit GEMM. Auto picks the tensor-core path when the shape
 // and epilogue are covered by it and an expanded filter is available, else LOP3+POPC.
@@ -59,6 +63,9 @@ struct TcFilter {
 // Returns the engine name used ("tc_i8" / "popc").
 const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e,
                          cudaStream_t st, EngineHint h, const TcFilter* tc = nullptr);
+
+// True when launch_bgemm would pick the tensor-core engine for (s, e).
+bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter* tc);
 
 // Tensor-core support (kernels_tc.cu).
 bool tc_supported(const ConvShape& s, const Epi& e);

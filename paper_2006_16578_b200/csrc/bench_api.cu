@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "api_internal.cuh"
+#include "bnmath.cuh"
 #include "layout.cuh"
 
 namespace btnn_gpu {
@@ -75,7 +76,30 @@ static void time_reps(int reps, int warmup, cudaStream_t st, F&& fn, double* med
 
 using namespace btnn_gpu;
 
+// Self-test of bnmath.cuh: the bn division with the per-channel reciprocal against
+// __ddiv_rn (and hence IEEE a/b) on caller-supplied operands.
+__global__ void div_selftest_kernel(const double* a, const double* b, size_t n, double* fast, double* ref) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double y = bn_recip(b[i]);
+    fast[i] = div_rn_with_recip(a[i], b[i], y);
+    ref[i] = __ddiv_rn(a[i], b[i]);
+  }
+}
+
 extern "C" {
+
+int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* fast, double* ref) {
+  return guard([&] {
+    cudaStream_t st = 0;
+    DevBuf da = upload(a, n, st), db = upload(b, n, st), df(n * 8), dr(n * 8);
+    div_selftest_kernel<<<1184, 256, 0, st>>>(da.get<double>(), db.get<double>(), n, df.get<double>(), dr.get<double>());
+    BT_CUDA(cudaGetLastError());
+    BT_CUDA(cudaMemcpyAsync(fast, df.get(), n * 8, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaMemcpyAsync(ref, dr.get(), n * 8, cudaMemcpyDeviceToHost, st));
+    BT_CUDA(cudaStreamSynchronize(st));
+  });
+}
+
 
 int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
                         size_t engine_len) {

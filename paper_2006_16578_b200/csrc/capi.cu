@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "api_internal.cuh"
+#include "bnmath.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 #include "layout.cuh"
@@ -89,7 +90,7 @@ void thresholds_to_int(const double* tau, const uint8_t* kind, size_t n, std::ve
 // add then IEEE sqrt, as BnParams::apply computes it), gamma, beta.
 void bn_to_device_arrays(const btnn_bn& bn, std::vector<double>& packed) {
   const size_t c = bn.channels;
-  packed.resize(4 * c);
+  packed.assign(kBnArrays * c, 0.0);
   for (size_t i = 0; i < c; ++i) {
     volatile double t = bn.var[i] + bn.eps;  // no contraction, no reassociation
     packed[i] = bn.mean[i];
@@ -98,6 +99,15 @@ void bn_to_device_arrays(const btnn_bn& bn, std::vector<double>& packed) {
     packed[3 * c + i] = bn.beta[i];
   }
 }
+DevBuf upload_bn(const btnn_bn& bn, cudaStream_t st) {
+  std::vector<double> p;
+  bn_to_device_arrays(bn, p);
+  DevBuf d = upload(p.data(), p.size(), st);
+  launch_bn_recip(d.get<double>(), (int)bn.channels, st);
+  BT_CUDA(cudaStreamSynchronize(st));  // the host staging vector dies here
+  return d;
+}
+
 // BnParams::validate (layer_math.hpp:19-30).
 void check_bn(const btnn_bn& bn) {
   require(bn.channels != 0 && bn.gamma && bn.beta && bn.mean && bn.var, BTNN_INVALID_INPUT,
@@ -542,10 +552,12 @@ int btnn_cuda_bconv_fused(const btnn_act_desc* in, const uint64_t* iw, const btn
       e.thr_hi = dhi.get<long long>();
     } else {
       dbn = upload(bnp.data(), bnp.size(), st);
+      launch_bn_recip(dbn.get<double>(), (int)O, st);
       e.bn_mean = dbn.get<double>();
       e.bn_s = e.bn_mean + O;
       e.bn_gamma = e.bn_mean + 2 * O;
       e.bn_beta = e.bn_mean + 3 * O;
+      e.bn_rcp = e.bn_mean + 4 * O;
     }
     if (fu->residual_in) {
       drin = upload(fu->residual_in, n_out, st);
@@ -602,7 +614,7 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
     DevBuf wb(first_conv_signbits_words((int)out_channels, K) * 4);
     launch_first_conv_signbits(dw.get<float>(), (int)out_channels, K, wb.get<uint32_t>(), st);
     a.wbits = wb.get<uint32_t>();
-    launch_first_conv(a, st);
+    if (!try_first_conv_tc_standalone(a, st)) launch_first_conv(a, st);
     BT_CUDA(cudaMemcpy(out, o.get(), n_out * 8, cudaMemcpyDeviceToHost));
   });
 }

@@ -20,14 +20,24 @@ static std::atomic<int> g_engine{engine_from_env()};
 
 int engine_override() { return g_engine.load(); }
 
+static EngineHint resolve(EngineHint h) {
+  if (h != EngineHint::Auto) return h;
+  const int o = g_engine.load();
+  return o == BTNN_ENGINE_POPC ? EngineHint::Popc : o == BTNN_ENGINE_TC ? EngineHint::TcI8 : EngineHint::Auto;
+}
+
+bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter* tc) {
+  h = resolve(h);
+  return h != EngineHint::Popc && tc && tc->valid() && tc_supported(s, e);
+}
+
 const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e, cudaStream_t st,
                          EngineHint h, const TcFilter* tc) {
-  if (h == EngineHint::Auto) {
-    const int o = g_engine.load();
-    h = o == BTNN_ENGINE_POPC ? EngineHint::Popc : o == BTNN_ENGINE_TC ? EngineHint::TcI8 : EngineHint::Auto;
-  }
+  h = resolve(h);
   const bool tc_ok = tc && tc->valid() && tc_supported(s, e);
   if (h == EngineHint::TcI8) require(tc_ok, BTNN_UNSUPPORTED_SHAPE, "tensor-core engine does not cover this shape");
+  require(e.rout_half == nullptr || (tc_ok && h != EngineHint::Popc), BTNN_CUDA_ERROR,
+          "halved tap output needs the tensor-core engine");
   if (tc_ok && h != EngineHint::Popc) {
     launch_bgemm_tc(s, act, *tc, e, st);
     return "tc_i8";

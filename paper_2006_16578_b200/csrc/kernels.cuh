@@ -38,9 +38,12 @@ struct Epi {
   const double* bn_s = nullptr;      //   s = sqrt(var + eps), computed on the host in IEEE f64
   const double* bn_gamma = nullptr;
   const double* bn_beta = nullptr;
+  const double* bn_rcp = nullptr;    //   per-channel reciprocal for the division (bnmath.cuh), optional
   const double* rin = nullptr;       // residual_in, PQNO over (rin_P, rin_Q, N, rin_C)
   int rin_P = 0, rin_Q = 0, rin_C = 0, rin_halve = 0;  // type-A adaptation (inference.hpp:43-63)
   double* rout = nullptr;            // residual_out / logits, PQNO over (P, Q, N, O)
+  double* rout_half = nullptr;       // residual_out pre-averaged for a halving consumer,
+                                     //   PQNO over (P/2, Q/2, N, O) (tensor-core engine only)
 };
 
 // CUDA-core LOP3+POPC implicit GEMM (any shape). act/filt are device pointers.
@@ -55,6 +58,7 @@ struct FirstConvArgs {
   double* out_acc;        // optional raw sums, PQNO (first_conv_bwn)
   // optional fused bn -> tap -> sign -> HWNC bits (run_inference's loop)
   const double *bn_mean, *bn_s, *bn_gamma, *bn_beta;
+  const double* bn_rcp = nullptr;  // optional per-channel reciprocal (bnmath.cuh)
   double* tap;            // optional, PQNO
   uint64_t* out_bits;     // optional, HWNC plain (pre-zeroed)
   int out_rps, cwo;
@@ -63,6 +67,18 @@ struct FirstConvArgs {
 void launch_first_conv(const FirstConvArgs& a, cudaStream_t st);
 size_t first_conv_signbits_words(int O, int K);
 void launch_first_conv_signbits(const float* w_pm1, int O, int K, uint32_t* out, cudaStream_t st);
+
+// Tensor-core first layer (kernels_first_tc.cu): exact integer-digit MMAs with a
+// sequential-f64 fix-up pass for windows whose terms do not fit the tile's grid.
+bool first_conv_tc_supported(const FirstConvArgs& a);
+size_t first_conv_tc_weight_bytes(int KH, int KW);
+void launch_first_conv_tc_weights(const float* w_pm1, int O, int KH, int KW, int C, int8_t* out, cudaStream_t st);
+// Input check per row (n, h) of W*C floats: non-finite flag + largest |x| bit pattern.
+void launch_input_rows(const float* x, size_t rows, int row_len, int* flag, uint32_t* rowmax, cudaStream_t st);
+// rowmax from launch_input_rows; fix_list holds up to N*P*Q window ids.
+void launch_first_conv_tc(const FirstConvArgs& a, const uint32_t* rowmax, const int8_t* wblk, int* fix_count,
+                          int* fix_list, cudaStream_t st);
+bool try_first_conv_tc_standalone(const FirstConvArgs& a, cudaStream_t st);
 
 // Format stage.
 void launch_check_finite(const float* x, size_t n, int* flag, cudaStream_t st);

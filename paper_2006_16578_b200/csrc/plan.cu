@@ -30,10 +30,15 @@ struct LayerDev {
   TcFilter tc;          // tensor-core operand (bit conv / fc when covered)
   DevBuf wpm1;          // first conv (o,r,s,c) floats
   DevBuf wbits;         // first conv per-o sign bits
+  DevBuf wblk;          // first conv tensor-core weight blocks (kernels_first_tc.cu)
+  DevBuf fix_list, fix_count;  // first conv windows left to the sequential kernel
   DevBuf thr_lo, thr_hi;
   DevBuf bn;            // mean | s | gamma | beta
   bool has_thr = false, has_bn = false;
   DevBuf tap;           // residual_out, PQNO f64 sized for max batch
+  DevBuf tap_half;      // residual_out pre-averaged 2x2 for a halving consumer (P/2, Q/2, N, O)
+  bool feeds_full = false, feeds_half = false;  // consumers read the tap as is / halved
+  bool wrote_half = false;                      // last enqueue stored tap_half instead of tap
   std::string engine = "-";
 };
 
@@ -43,6 +48,7 @@ struct Shard {
   size_t max_batch = 0;
   std::vector<LayerDev> layers;
   DevBuf x, act[2], fc[2], logits, labels, flag;
+  DevBuf rowmax;        // per input row (n, h): largest |x| (tensor-core first conv)
   size_t act_words = 0, fc_words = 0;
   std::map<std::tuple<size_t, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
   std::vector<cudaEvent_t> events;  // breakdown
@@ -164,6 +170,12 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
       const int K = (int)(l.kh * l.kw * l.in_channels);
       L.wbits.alloc(first_conv_signbits_words((int)l.out_channels, K) * 4);
       launch_first_conv_signbits(L.wpm1.get<float>(), (int)l.out_channels, K, L.wbits.get<uint32_t>(), st);
+      L.wblk.alloc(first_conv_tc_weight_bytes((int)l.kh, (int)l.kw));
+      launch_first_conv_tc_weights(L.wpm1.get<float>(), (int)l.out_channels, (int)l.kh, (int)l.kw,
+                                   (int)l.in_channels, L.wblk.get<int8_t>(), st);
+      L.fix_list.alloc(B * l.out_h * l.out_w * sizeof(int));
+      L.fix_count.alloc(sizeof(int));
+      sh.rowmax.alloc(B * l.in_h * sizeof(uint32_t));
     } else if (l.kind == BTNN_BIT_CONV) {
       DevBuf raw = upload(w.filter_words, w.filter_n_words, st);
       if (!ws->tiled) {
@@ -195,13 +207,24 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
         L.thr_hi = upload(hi.data(), hi.size(), st);
         L.has_thr = true;
       } else {
-        std::vector<double> p;
-        bn_to_device_arrays(w.bn, p);
-        L.bn = upload(p.data(), p.size(), st);
+        L.bn = upload_bn(w.bn, st);
         L.has_bn = true;
       }
     }
-    if (l.residual_out) L.tap.alloc(l.out_h * l.out_w * B * l.out_channels * sizeof(double));
+    if (l.residual_out) {
+      // Who reads this tap: adapt_shortcut halves it when the consumer's grid is smaller
+      // (inference.hpp:46). A producer whose every consumer halves may store only the
+      // pre-averaged tap (kernels_tc.cu, blocked row order); the full one stays allocated
+      // for engines or grids that cannot.
+      for (size_t j = i + 1; j < m->n_layers; ++j) {
+        const btnn_layer_spec& c = m->layers[j];
+        if (!c.residual_in || c.shortcut_from != (int)i) continue;
+        (c.out_h != l.out_h ? L.feeds_half : L.feeds_full) = true;
+      }
+      L.tap.alloc(l.out_h * l.out_w * B * l.out_channels * sizeof(double));
+      if (L.feeds_half && !L.feeds_full && l.kind == BTNN_BIT_CONV && l.out_h % 2 == 0 && l.out_w % 2 == 0)
+        L.tap_half.alloc((l.out_h / 2) * (l.out_w / 2) * B * l.out_channels * sizeof(double));
+    }
     BT_CUDA(cudaStreamSynchronize(st));  // host staging vectors die here
   }
   sh.act_words = act_max;
@@ -224,7 +247,22 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
   cudaStream_t st = sh.stream;
   size_t launches = 0;
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), st));
-  launch_check_finite(d_x, batch * plan->in_h * plan->in_w * plan->in_c, sh.flag.get<int>(), st);
+  // The tensor-core first conv needs per-row input maxima; that input pass doubles as the
+  // non-finite check (inference.hpp:69-75).
+  FirstConvArgs fa{};
+  bool first_tc = false;
+  if (!sh.layers.empty() && sh.layers[0].spec.kind == BTNN_FIRST_CONV_BWN) {
+    const btnn_layer_spec& l = sh.layers[0].spec;
+    fa.N = (int)batch; fa.H = (int)l.in_h; fa.W = (int)l.in_w; fa.C = (int)l.in_channels; fa.O = (int)l.out_channels;
+    fa.KH = (int)l.kh; fa.KW = (int)l.kw; fa.stride = (int)l.stride; fa.pad = (int)l.pad;
+    fa.P = (int)l.out_h; fa.Q = (int)l.out_w;
+    first_tc = engine_override() != BTNN_ENGINE_POPC && first_conv_tc_supported(fa);
+  }
+  if (first_tc)
+    launch_input_rows(d_x, batch * plan->in_h, (int)(plan->in_w * plan->in_c), sh.flag.get<int>(),
+                      sh.rowmax.get<uint32_t>(), st);
+  else
+    launch_check_finite(d_x, batch * plan->in_h * plan->in_w * plan->in_c, sh.flag.get<int>(), st);
   ++launches;
   const size_t np = act_npad(batch, 0, 0);
   int cur = 0;              // act buffer holding the current activations
@@ -246,14 +284,22 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       a.P = (int)l.out_h; a.Q = (int)l.out_w;
       const size_t C4 = l.out_channels;
       a.bn_mean = L.bn.get<double>(); a.bn_s = a.bn_mean + C4; a.bn_gamma = a.bn_mean + 2 * C4; a.bn_beta = a.bn_mean + 3 * C4;
+      a.bn_rcp = a.bn_mean + 4 * C4;
       a.tap = l.residual_out ? L.tap.get<double>() : nullptr;
       a.out_bits = out;
       a.wbits = L.wbits.get<uint32_t>();
       a.out_rps = (int)np;
       a.cwo = (int)(act_cpad(l.out_channels, 0, 0) / 64);
-      launch_first_conv(a, st);
-      ++launches;
-      L.engine = "fp64";
+      if (first_tc) {
+        launch_first_conv_tc(a, sh.rowmax.get<uint32_t>(), L.wblk.get<int8_t>(), L.fix_count.get<int>(),
+                             L.fix_list.get<int>(), st);
+        launches += 2;
+        L.engine = "tc_i8_exact";
+      } else {
+        launch_first_conv(a, st);
+        ++launches;
+        L.engine = "fp64";
+      }
       H = l.out_h; W = l.out_w; C = l.out_channels;
     } else if (l.kind == BTNN_BIT_CONV) {
       const uint64_t* in = sh.act[cur].get<uint64_t>();
@@ -269,16 +315,36 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       } else {
         const size_t O = l.out_channels;
         e.bn_mean = L.bn.get<double>(); e.bn_s = e.bn_mean + O; e.bn_gamma = e.bn_mean + 2 * O; e.bn_beta = e.bn_mean + 3 * O;
+        e.bn_rcp = e.bn_mean + 4 * O;
       }
       if (l.residual_in) {
         const LayerDev& src = sh.layers[l.shortcut_from];
-        e.rin = src.tap.get<double>();
-        e.rin_P = (int)src.spec.out_h;
-        e.rin_Q = (int)src.spec.out_w;
         e.rin_C = (int)src.spec.out_channels;
-        e.rin_halve = src.spec.out_h != l.out_h;  // adapt_shortcut's `halve` (inference.hpp:46)
+        if (src.wrote_half) {  // already averaged by the producer: read as is
+          e.rin = src.tap_half.get<double>();
+          e.rin_P = (int)l.out_h;
+          e.rin_Q = (int)l.out_w;
+          e.rin_halve = 0;
+        } else {
+          e.rin = src.tap.get<double>();
+          e.rin_P = (int)src.spec.out_h;
+          e.rin_Q = (int)src.spec.out_w;
+          e.rin_halve = src.spec.out_h != l.out_h;  // adapt_shortcut's `halve` (inference.hpp:46)
+        }
       }
-      if (l.residual_out) e.rout = L.tap.get<double>();
+      L.wrote_half = false;
+      if (l.residual_out) {
+        e.rout = L.tap.get<double>();
+        if (L.tap_half.get()) {
+          Epi eh = e;
+          eh.rout = nullptr;
+          eh.rout_half = L.tap_half.get<double>();
+          if (will_use_tc(s, eh, EngineHint::Auto, &L.tc)) {
+            e = eh;
+            L.wrote_half = true;
+          }
+        }
+      }
       L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
       ++launches;
       cur ^= 1;
@@ -323,6 +389,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         const size_t O = l.units;
         e.mode = EPI_F64;
         e.bn_mean = L.bn.get<double>(); e.bn_s = e.bn_mean + O; e.bn_gamma = e.bn_mean + 2 * O; e.bn_beta = e.bn_mean + 3 * O;
+        e.bn_rcp = e.bn_mean + 4 * O;
         e.rout = d_logits;  // logits = bn(v) (inference.hpp:161-164)
         L.engine = launch_bgemm(s, sh.fc[fcur].get<uint64_t>(), L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
       }
@@ -511,8 +578,23 @@ int btnn_cuda_plan_read_tap(btnn_plan* plan, size_t i, size_t batch, double* out
     require(batch > 0 && batch <= sh.max_batch, BTNN_INVALID_INPUT, "plan_read_tap: bad batch");
     BT_CUDA(cudaSetDevice(sh.device));
     BT_CUDA(cudaStreamSynchronize(sh.stream));
-    BT_CUDA(cudaMemcpy(out, L.tap.get(), L.spec.out_h * L.spec.out_w * batch * L.spec.out_channels * sizeof(double),
-                       cudaMemcpyDeviceToHost));
+    // The tap as the last run stored it: full resolution, or pre-averaged (see tap_dims).
+    const size_t hw = L.wrote_half ? (L.spec.out_h / 2) * (L.spec.out_w / 2) : L.spec.out_h * L.spec.out_w;
+    BT_CUDA(cudaMemcpy(out, L.wrote_half ? L.tap_half.get() : L.tap.get(),
+                       hw * batch * L.spec.out_channels * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int btnn_cuda_plan_tap_dims(btnn_plan* plan, size_t i, size_t* dims) {
+  return guard([&] {
+    require(plan && !plan->shards.empty() && i < plan->specs.size() && dims, BTNN_INVALID_INPUT,
+            "plan_tap_dims: bad layer");
+    const LayerDev& L = plan->shards[0]->layers[i];
+    require(L.spec.residual_out, BTNN_INVALID_INPUT, "plan_tap_dims: layer has no residual_out");
+    dims[0] = L.wrote_half ? L.spec.out_h / 2 : L.spec.out_h;
+    dims[1] = L.wrote_half ? L.spec.out_w / 2 : L.spec.out_w;
+    dims[2] = L.wrote_half ? 1 : 0;  // 1: 2x2-averaged (adapt_shortcut's halve, inference.hpp:43-63)
+    dims[3] = L.spec.out_channels;
   });
 }
 

@@ -204,3 +204,29 @@ def test_error_classes_match_reference():  # test_bmm.cpp:156-174, test_bconv.cp
         B.bconv_pm1(capi.ActDesc(2, 2, 1, 16, 0, 8, 128), np.zeros(16, np.uint64), fd, np.zeros(144, np.uint64),
                     capi.ConvGeom(3, 3, 1, 0))
     assert e.value.code == capi.BTNN_UNSUPPORTED_SHAPE
+
+
+def test_bn_division_matches_ddiv_rn():
+    """bnmath.cuh: the per-channel-reciprocal division equals __ddiv_rn and IEEE a/b
+    bit for bit — bn-route operands (integer v - mean over s = sqrt(var + eps)), random
+    doubles over a wide exponent range, and the range edges where __ddiv_rn leaves its
+    fast path (zeros, tiny and huge quotients)."""
+    rng = np.random.default_rng(5)
+    n = 1 << 20
+    s = np.sqrt(rng.uniform(0.25, 2.0, n) + 1e-5)
+    v = rng.integers(-4608, 4609, n).astype(np.float64)
+    mean = rng.standard_normal(n) * np.sqrt(4608) / 2
+    a1, b1 = v - mean, s
+    a2 = rng.standard_normal(n) * np.exp2(rng.integers(-1000, 1000, n).astype(np.float64))
+    b2 = np.abs(rng.standard_normal(n)) * np.exp2(rng.integers(-60, 60, n).astype(np.float64)) + 1e-300
+    edge = np.array([0.0, -0.0, 5e-324, -5e-324, 2.0**-1022, 2.0**-900, 2.0**-899, 1.0, -1.0, 1e300, -1e300, 2.0**1000])
+    a3 = np.repeat(edge, 8)
+    b3 = np.tile(np.array([1.0, 3.0, 1e-3, 0.7, 2.0**-60, 2.0**60, 1e-300, 1e300]), edge.size)
+    a, b = np.concatenate([a1, a2, a3]), np.concatenate([b1, b2, b3])
+    fast, ref = np.zeros_like(a), np.zeros_like(a)
+    capi.check(capi.lib().btnn_cuda_selftest_div(ptr(a, C.c_double), ptr(b, C.c_double), a.size,
+                                                 ptr(fast, C.c_double), ptr(ref, C.c_double)))
+    with np.errstate(all="ignore"):
+        want = a / b
+    assert np.array_equal(ref.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(fast.view(np.uint64), want.view(np.uint64))

@@ -103,3 +103,26 @@ def _ref_run(m, ws, x):
                              ptr(lg, C.c_double), ptr(lb, C.c_int32))
     assert st == 0, ref().ref_last_error()
     return lg.reshape(x.shape[0], m.classes), lb
+
+
+def test_halved_tap_equals_adapt_shortcut():
+    """A layer whose tap only feeds a halving shortcut stores the 2x2 average directly
+    (tensor-core engine, blocked row order). It must equal adapt_shortcut's
+    ((a+b)+c)+d)*0.25 (inference.hpp:43-63) of the full tap the CUDA-core engine stores,
+    including a batch that is not a multiple of the 32-image row group."""
+    m = M.make_model("halve", "16C3-32C3-32C3-64C3/2-64C3", 12, 12, 3, 5, [(0, 2), (2, 4)])
+    ws = Wt.build_weights(m, Wt.random_weights(m, 31))
+    x = np.random.default_rng(32).standard_normal((37, 12, 12, 3), dtype=np.float32)
+    capi.set_engine(capi.ENGINE_POPC)
+    p_full = B.Plan(m, ws, 37)
+    lg_full, _ = p_full.run(x)
+    full = p_full.read_tap(2, 37).reshape(12, 12, 37, 32)
+    capi.set_engine(capi.ENGINE_TC)
+    p_half = B.Plan(m, ws, 37)
+    lg_half, _ = p_half.run(x)
+    assert p_half.tap_dims(2) == (6, 6, 1, 32)
+    half = p_half.read_tap(2, 37).reshape(6, 6, 37, 32)
+    a, b, c, d = full[0::2, 0::2], full[0::2, 1::2], full[1::2, 0::2], full[1::2, 1::2]
+    want = (((a + b) + c) + d) * 0.25
+    assert np.array_equal(half.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(lg_half.view(np.uint64), lg_full.view(np.uint64))
