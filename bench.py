@@ -109,6 +109,16 @@ def roofline(m, B, i, ms, engine):
     hbm = peaks().get("hbm_gbs")
     pk = engine_peaks()
     sec = ms / 1e3
+    if L.kind == 0 and engine.startswith("tc_i8"):
+        # tensor-core first layer (exact integer digits): HBM-bound on its algorithmic bytes —
+        # the f32 input read once, the f64 tap and the packed output bits written once.
+        byts = B * (4.0 * L.in_h * L.in_w * L.in_channels
+                    + (8.0 * L.out_h * L.out_w * L.out_channels if L.residual_out else 0.0)
+                    + L.out_h * L.out_w * ((L.out_channels + 127) // 128) * 16.0)
+        a = byts / sec / 1e9
+        return {"bound": "hbm", "kernel": f"layer{i}:{engine}", "achieved": a, "peak": hbm, "unit": "GB/s",
+                "frac": a / hbm if hbm else None, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "note": "f32 input + f64 tap + bits per image (DESIGN.md §3)"}
     if L.kind == 0:  # f64 first layer: 2 flops per tap term
         flops = 2.0 * L.out_h * L.out_w * B * L.in_channels * L.out_channels * L.kh * L.kw
         a = flops / sec / 1e12

@@ -24,6 +24,8 @@
 
 namespace btnn_gpu {
 
+constexpr size_t kChunk = 128, kMaxChunks = 8;  // run_shard_host's input pipelining
+
 struct LayerDev {
   btnn_layer_spec spec{};
   DevBuf filt;          // plain KKOC filter / ColPacked fc matrix
@@ -52,12 +54,16 @@ struct Shard {
   size_t act_words = 0, fc_words = 0;
   std::map<std::tuple<size_t, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
   std::vector<cudaEvent_t> events;  // breakdown
+  cudaStream_t copy_stream = nullptr;    // host->device input chunks (run_shard_host)
+  std::vector<cudaEvent_t> in_ready;     // per chunk: input resident
   size_t launches = 0;
   ~Shard() {
     if (device >= 0) cudaSetDevice(device);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
     for (auto ev : events) cudaEventDestroy(ev);
+    for (auto ev : in_ready) cudaEventDestroy(ev);
     if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
   }
 };
 
@@ -150,6 +156,7 @@ static void check_plan_inputs(const btnn_model_spec* m, const btnn_weight_store*
 static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_store* ws) {
   BT_CUDA(cudaSetDevice(sh.device));
   BT_CUDA(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+  BT_CUDA(cudaStreamCreateWithFlags(&sh.copy_stream, cudaStreamNonBlocking));
   cudaStream_t st = sh.stream;
   const size_t B = sh.max_batch;
   sh.layers.resize(m->n_layers);
@@ -237,6 +244,8 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
   sh.flag.alloc(sizeof(int));
   sh.events.resize(m->n_layers + 1);
   for (auto& ev : sh.events) BT_CUDA(cudaEventCreate(&ev));
+  sh.in_ready.resize(kMaxChunks);
+  for (auto& ev : sh.in_ready) BT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   BT_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -246,7 +255,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
                               int32_t* d_labels, bool timed) {
   cudaStream_t st = sh.stream;
   size_t launches = 0;
-  BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), st));
+  // (sh.flag is cleared by the host-side caller, so one flag covers all chunks of a run.)
   // The tensor-core first conv needs per-row input maxima; that input pass doubles as the
   // non-finite check (inference.hpp:69-75).
   FirstConvArgs fa{};
@@ -433,12 +442,30 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
   BT_CUDA(cudaGraphLaunch(it->second, launch_stream ? launch_stream : sh.stream));
 }
 
+// Host-buffer run (the C ABI's run_inference). The input copy is the long pole
+// end to end (602 KB per ImageNet image over PCIe), so the batch is cut into chunks of
+// ~kChunk images: chunk k+1's host->device copy runs on the copy stream while chunk k's
+// graph runs on the compute stream. Samples are independent, so chunking does not change
+// any result.
+
 static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t batch, double* logits, int32_t* labels) {
   BT_CUDA(cudaSetDevice(sh.device));
-  const size_t xin = batch * plan->in_h * plan->in_w * plan->in_c;
-  BT_CUDA(cudaMemcpyAsync(sh.x.get(), x, xin * sizeof(float), cudaMemcpyHostToDevice, sh.stream));
-  run_shard_device(plan, sh, sh.x.get<float>(), batch, sh.logits.get<double>(), sh.labels.get<int32_t>(),
-                   plan->breakdown && &sh == plan->shards[0].get());
+  const size_t xin = plan->in_h * plan->in_w * plan->in_c;
+  const bool timed = plan->breakdown && &sh == plan->shards[0].get();
+  const size_t nch = timed ? 1 : std::max<size_t>(1, std::min(kMaxChunks, batch / kChunk));
+  const size_t per = cdiv(batch, nch);
+  BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
+  for (size_t k = 0; k < nch; ++k) {
+    const size_t b0 = k * per;
+    if (b0 >= batch) break;
+    const size_t bn = std::min(per, batch - b0);
+    float* dx = sh.x.get<float>() + b0 * xin;
+    BT_CUDA(cudaMemcpyAsync(dx, x + b0 * xin, bn * xin * sizeof(float), cudaMemcpyHostToDevice, sh.copy_stream));
+    BT_CUDA(cudaEventRecord(sh.in_ready[k], sh.copy_stream));
+    BT_CUDA(cudaStreamWaitEvent(sh.stream, sh.in_ready[k], 0));
+    run_shard_device(plan, sh, dx, bn, sh.logits.get<double>() + b0 * plan->classes, sh.labels.get<int32_t>() + b0,
+                     timed);
+  }
   int bad = 0;
   BT_CUDA(cudaMemcpyAsync(&bad, sh.flag.get(), sizeof(int), cudaMemcpyDeviceToHost, sh.stream));
   BT_CUDA(cudaMemcpyAsync(logits, sh.logits.get(), batch * plan->classes * sizeof(double), cudaMemcpyDeviceToHost,

@@ -230,3 +230,42 @@ def test_bn_division_matches_ddiv_rn():
         want = a / b
     assert np.array_equal(ref.view(np.uint64), want.view(np.uint64))
     assert np.array_equal(fast.view(np.uint64), want.view(np.uint64))
+
+
+def _oracle_first_conv(x, wpm, k, o, s, pd):
+    n, h, w, c = x.shape
+    P, Q = (h + 2 * pd - k) // s + 1, (w + 2 * pd - k) // s + 1
+    want = np.zeros(P * Q * n * o)
+    geo = capi.ConvGeom(k, k, s, pd)
+    st = oracle().bo_first_conv_bwn(ptr(np.ascontiguousarray(x), C.c_float), n, h, w, c,
+                                    ptr(np.ascontiguousarray(wpm), C.c_float), k, k, o, C.byref(geo),
+                                    ptr(want, C.c_double))
+    assert st == 0
+    return want
+
+
+@pytest.mark.parametrize("n,hw,k,o,pd", [(3, 224, 7, 64, 3), (2, 61, 11, 48, 5), (4, 36, 5, 16, 2)])
+def test_first_conv_exact_digits_adversarial(n, hw, k, o, pd):
+    """The tensor-core first layer (integer digit MMAs, kernels_first_tc.cu) is exact only
+    on a per-tile grid; inputs here put values off that grid (tiny and subnormal values
+    next to large ones, signed zeros, powers of two, an all-zero image, a huge outlier) so
+    the sequential-f64 fix-up pass runs, and every output must still equal the
+    reference's sequential sum bit for bit."""
+    rng = np.random.default_rng(77 + hw)
+    x = rng.standard_normal((n, hw, hw, 3)).astype(np.float32)
+    flat = x.reshape(n, -1)
+    m = flat.shape[1]
+    idx = rng.integers(0, m, 40)
+    flat[0, idx[:10]] = np.float32(1e-12)
+    flat[0, idx[10:14]] = np.float32(-3e-39)  # subnormal
+    flat[0, idx[14:18]] = -0.0
+    flat[0, idx[18:22]] = np.exp2(rng.integers(-30, 10, 4)).astype(np.float32)
+    flat[1, :] = 0.0
+    flat[1, idx[22:26]] = np.float32(7.5e-8)
+    if n > 2:
+        flat[2, idx[26]] = np.float32(3e20)
+        flat[2, idx[27:40]] = rng.standard_normal(13).astype(np.float32) * np.float32(1e-6)
+    wpm = np.where(rng.standard_normal(o * k * k * 3) >= 0, 1.0, -1.0).astype(np.float32)
+    got = B.first_conv_bwn(x, wpm, k, k, o, capi.ConvGeom(k, k, 4, pd))
+    want = _oracle_first_conv(x, wpm, k, o, 4, pd)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
