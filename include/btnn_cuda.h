@@ -166,6 +166,10 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
 int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t window,
                       size_t stride, uint64_t* out_words);
 
+/* Timing experiments only: copies the per-K-step clock64 stamps recorded by CTA 0 of the
+ * last tensor-core GEMM launched with BTNN_TC_DBG & 16 (n <= 4096 entries). */
+int btnn_cuda_debug_tc_timestamps(unsigned long long* out, size_t n);
+
 /* Self-test of the bn-route division (csrc/bnmath.cuh): fast[i] = a[i]/b[i] through the
  * per-channel-reciprocal path, ref[i] = __ddiv_rn(a[i], b[i]); host buffers of n doubles. */
 int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* fast, double* ref);

@@ -19,15 +19,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting thread sleeps until the phase completes (or
+// the hint expires) instead of spinning, so idle roles do not take issue slots from the
+// producers and the epilogue.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "LAB_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra LAB_WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000)
       : "memory");
 }
 
@@ -103,6 +106,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 #define UMMA_R8(p) "=r"(v[p]), "=r"(v[p + 1]), "=r"(v[p + 2]), "=r"(v[p + 3]), "=r"(v[p + 4]), "=r"(v[p + 5]), "=r"(v[p + 6]), "=r"(v[p + 7])
 #define UMMA_W8(p) "r"(v[p]), "r"(v[p + 1]), "r"(v[p + 2]), "r"(v[p + 3]), "r"(v[p + 4]), "r"(v[p + 5]), "r"(v[p + 6]), "r"(v[p + 7])
 
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : UMMA_R8(0)
