@@ -170,6 +170,10 @@ int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t 
  * last tensor-core GEMM launched with BTNN_TC_DBG & 16 (n <= 4096 entries). */
 int btnn_cuda_debug_tc_timestamps(unsigned long long* out, size_t n);
 
+/* Timing experiments only: per-tile clock64 stamps of CTA 0 of the last tensor-core first
+ * layer launched with BTNN_FTC_DBG=1 (n <= 512 entries, 8 per tile). */
+int btnn_cuda_debug_ftc_timestamps(unsigned long long* out, size_t n);
+
 /* Self-test of the bn-route division (csrc/bnmath.cuh): fast[i] = a[i]/b[i] through the
  * per-channel-reciprocal path, ref[i] = __ddiv_rn(a[i], b[i]); host buffers of n doubles. */
 int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* fast, double* ref);

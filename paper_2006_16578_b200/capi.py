@@ -123,6 +123,7 @@ _PROTOS = {
     "btnn_cuda_plan_tap_dims": (C.c_int, [C.c_void_p, sz, P(sz)]),
     "btnn_cuda_selftest_div": (C.c_int, [f64p, f64p, sz, f64p, f64p]),
     "btnn_cuda_debug_tc_timestamps": (C.c_int, [P(C.c_uint64), sz]),
+    "btnn_cuda_debug_ftc_timestamps": (C.c_int, [P(C.c_uint64), sz]),
     "btnn_cuda_plan_layer_engine": (C.c_char_p, [C.c_void_p, sz]),
     "btnn_cuda_plan_destroy": (C.c_int, [C.c_void_p]),
 }

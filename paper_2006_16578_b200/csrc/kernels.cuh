@@ -23,6 +23,8 @@ struct ConvShape {
   int O;                 // logical output channels
   int f_rps;             // filter rows per tap plane (o_pad)
   int cwo;               // u64 words per output bit row (out c_pad / 64)
+  int halo_ok = 0;       // layer may use the halo-mode tensor-core kernel (fixes the filter layout;
+                         // set for threshold-route convs with C <= 128, where it is faster)
 };
 
 // Fused epilogue (bconv.hpp:160-194, bmm.hpp:219-274, inference.hpp:107-118/161-164).

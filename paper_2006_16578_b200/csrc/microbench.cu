@@ -89,6 +89,44 @@ __global__ void probe_kernel(int32_t* out_ts, int32_t* out_ss) {
   if (warp == 0) tmem_dealloc(tb, 64);
 }
 
+// SS-mode with the halo kernel's SWIZZLE_64B layout: rows of 64 B, iters x 4 MMAs that
+// alternate the two 32-byte K halves of the row.
+template <int N>
+__global__ void __launch_bounds__(128, 1) tc_sw64_kernel(int iters, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* as = smem;             // 128 x 64 bytes
+  uint8_t* bs = smem + 128 * 64;  // N x 64 bytes
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  for (int i = tid; i < (128 + N) * 64 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x01010101u, 0, 0, 0);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tb = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(128, N);
+    const uint64_t ad = sdesc_sw(smem_u32(as), 64), bd = sdesc_sw(smem_u32(bs), 64);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mma_i8_ss(tb, ad + 2 * (j & 1), bd + 2 * (j & 1), id, 1);
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tb, 512);
+}
+
 // tcgen05 i8 throughput: one thread issues iters x 4 MMAs (M128 x N x K32) back to back.
 template <bool ATMEM, int N>
 __global__ void __launch_bounds__(128, 1) tc_peak_kernel(int iters, long long* cycles) {
@@ -289,6 +327,10 @@ int main() {
   tc(tc_peak_kernel<false, 256>, 256, false, "tc_i8_smemA_n256");
   tc(tc_peak_kernel<true, 128>, 128, true, "tc_i8_tmemA_n128");
   tc(tc_peak_kernel<true, 64>, 64, true, "tc_i8_tmemA_n64");
+  tc(tc_peak_kernel<false, 128>, 128, false, "tc_i8_smemA_n128");
+  tc(tc_peak_kernel<false, 64>, 64, false, "tc_i8_smemA_n64");
+  tc(tc_sw64_kernel<64>, 64, false, "tc_i8_smemA_sw64_n64");
+  tc(tc_sw64_kernel<128>, 128, false, "tc_i8_smemA_sw64_n128");
 
   // ---- legacy warp MMA, popc, fp64: grid 148*8 blocks x 256 threads
   const int blocks = sms * 8, threads = 256, it = 2048;

@@ -80,8 +80,9 @@ struct btnn_plan {
 
 namespace btnn_gpu {
 
-static ConvShape conv_shape(const btnn_layer_spec& l, size_t batch) {
+static ConvShape conv_shape(const btnn_layer_spec& l, size_t batch, bool thr_route) {
   ConvShape s{};
+  s.halo_ok = thr_route && l.in_channels <= 128;
   s.P = (int)l.out_h; s.Q = (int)l.out_w;
   s.H = (int)l.in_h; s.W = (int)l.in_w;
   s.KH = (int)l.kh; s.KW = (int)l.kw; s.stride = (int)l.stride; s.pad = (int)l.pad;
@@ -193,7 +194,8 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
                            L.filt.get<uint64_t>(), st);
         BT_CUDA(cudaStreamSynchronize(st));
       }
-      tc_prepare_filter(conv_shape(l, B), L.filt.get<uint64_t>(), L.tc, st);
+      const bool thr_route = w.n_thresholds && !(l.residual_in || l.residual_out);
+      tc_prepare_filter(conv_shape(l, B, thr_route), L.filt.get<uint64_t>(), L.tc, st);
     } else if (l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC) {
       DevBuf raw = upload(w.fc_words, w.fc_n_words, st);
       if (!ws->tiled) {
@@ -314,7 +316,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       const uint64_t* in = sh.act[cur].get<uint64_t>();
       uint64_t* out = sh.act[cur ^ 1].get<uint64_t>();
       BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
-      const ConvShape s = conv_shape(l, batch);
+      const ConvShape s = conv_shape(l, batch, L.has_thr);
       Epi e;
       e.mode = EPI_BITS;
       e.out_bits = out;

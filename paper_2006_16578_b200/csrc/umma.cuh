@@ -72,6 +72,24 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)1 << 46;  // descriptor version (sm_100)
   return d;                // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE
 }
+// K-major descriptor for the hardware-swizzled layouts: rows of rb = 32/64/128 bytes
+// (SWIZZLE_32B/64B/128B), 8-row atoms of 8*rb bytes (SBO), 16-byte chunk c of row r stored
+// at chunk c ^ ((r >> s) & m) with (s, m) = (2, 1) / (1, 3) / (0, 7). The atom base must be
+// aligned to 8*rb; advancing K inside a row adds the byte offset to the start address.
+__device__ __forceinline__ uint64_t sdesc_sw(uint32_t saddr, uint32_t rb) {
+  const uint64_t type = rb == 128 ? 2u : rb == 64 ? 4u : 6u;
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;                              // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(((8 * rb) >> 4) & 0x3FFFu) << 32;    // SBO: one 8-row atom
+  d |= (uint64_t)1 << 46;
+  d |= type << 61;
+  return d;
+}
+__host__ __device__ __forceinline__ uint32_t sw_chunk(uint32_t row, uint32_t chunk, uint32_t rb) {
+  return rb == 128 ? (chunk ^ (row & 7u)) : rb == 64 ? (chunk ^ ((row >> 1) & 3u)) : (chunk ^ ((row >> 2) & 1u));
+}
+
 // Instruction descriptor, kind::i8: D s32, A s8, B s8, both K-major, dense.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -96,6 +114,31 @@ __device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-wide variants: the whole warp runs the issue loop (so descriptors and loop state
+// stay in uniform registers) and elect.sync picks the one lane that issues.
+__device__ __forceinline__ void mma_i8_ss_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_i8_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // Arrive on an mbarrier once every previously issued MMA of this thread completes.
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))

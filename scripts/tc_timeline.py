@@ -32,3 +32,9 @@ print(" top->issued issued->cpwait cpwait->expanded expanded->stwait stwait->arr
 for r in range(39):
     d = np.diff(np.append(it[r], it[r + 1][0]))
     print(r + 10, d.tolist())
+h = ts[3072:3072 + 800].astype(np.int64).reshape(100, 8)
+if h[:, 0].any():
+    hb = h[h > 0].min()
+    print("halo units: start freed built | mma_start mma_issued   (clk)")
+    for u in range(24):
+        print(u, (h[u, :5] - hb).tolist())
