@@ -208,7 +208,7 @@ int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, siz
       e.mode = EPI_I32;
       e.out_i32 = out_i.get<int32_t>();
     }
-    s.halo_ok = e.bn_mean == nullptr && s.C <= 128;
+    s.halo_ok = s.C <= 128;
     TcFilter tcf;
     if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, filt.get<uint64_t>(), tcf, st);
     const char* used = "popc";

@@ -188,7 +188,7 @@ static void use_device() { BT_CUDA(cudaSetDevice(g_device)); }
 static const char* run_gemm(const ConvShape& s0, const uint64_t* act, const uint64_t* filt, const Epi& e,
                             cudaStream_t st) {
   ConvShape s = s0;
-  s.halo_ok = e.bn_mean == nullptr && s.C <= 128;
+  s.halo_ok = s.C <= 128;
   TcFilter tcf;
   if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, filt, tcf, st);
   const char* engine = launch_bgemm(s, act, filt, e, st, EngineHint::Auto, &tcf);

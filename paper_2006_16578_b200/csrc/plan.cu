@@ -41,6 +41,7 @@ struct LayerDev {
   DevBuf tap_half;      // residual_out pre-averaged 2x2 for a halving consumer (P/2, Q/2, N, O)
   bool feeds_full = false, feeds_half = false;  // consumers read the tap as is / halved
   bool wrote_half = false;                      // last enqueue stored tap_half instead of tap
+  bool halo_ok = false;                         // conv may run the halo-mode kernel (filter layout)
   std::string engine = "-";
 };
 
@@ -80,9 +81,9 @@ struct btnn_plan {
 
 namespace btnn_gpu {
 
-static ConvShape conv_shape(const btnn_layer_spec& l, size_t batch, bool thr_route) {
+static ConvShape conv_shape(const btnn_layer_spec& l, size_t batch, bool halo_ok) {
   ConvShape s{};
-  s.halo_ok = thr_route && l.in_channels <= 128;
+  s.halo_ok = halo_ok && l.in_channels <= 128;
   s.P = (int)l.out_h; s.Q = (int)l.out_w;
   s.H = (int)l.in_h; s.W = (int)l.in_w;
   s.KH = (int)l.kh; s.KW = (int)l.kw; s.stride = (int)l.stride; s.pad = (int)l.pad;
@@ -194,8 +195,14 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
                            L.filt.get<uint64_t>(), st);
         BT_CUDA(cudaStreamSynchronize(st));
       }
-      const bool thr_route = w.n_thresholds && !(l.residual_in || l.residual_out);
-      tc_prepare_filter(conv_shape(l, B, thr_route), L.filt.get<uint64_t>(), L.tc, st);
+      // Halo-mode kernels for every conv except a tap producer whose consumer halves it
+      // (that one writes the pre-averaged tap in 2x2-blocked row order, TMEM-A path).
+      L.halo_ok = true;
+      if (l.residual_out)
+        for (size_t j = i + 1; j < m->n_layers; ++j)
+          if (m->layers[j].residual_in && m->layers[j].shortcut_from == (int)i && m->layers[j].out_h != l.out_h)
+            L.halo_ok = false;
+      tc_prepare_filter(conv_shape(l, B, L.halo_ok), L.filt.get<uint64_t>(), L.tc, st);
     } else if (l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC) {
       DevBuf raw = upload(w.fc_words, w.fc_n_words, st);
       if (!ws->tiled) {
@@ -316,7 +323,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       const uint64_t* in = sh.act[cur].get<uint64_t>();
       uint64_t* out = sh.act[cur ^ 1].get<uint64_t>();
       BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
-      const ConvShape s = conv_shape(l, batch, L.has_thr);
+      const ConvShape s = conv_shape(l, batch, L.halo_ok);
       Epi e;
       e.mode = EPI_BITS;
       e.out_bits = out;
