@@ -32,3 +32,8 @@ print("epilogue tiles (start, end, dur):")
 for i in range(16):
     if ep[i, 0]:
         print(i, int(ep[i, 0] - t0), int(ep[i, 1] - t0), int(ep[i, 1] - ep[i, 0]))
+h = t[3072:3072 + 800].reshape(100, 8)
+if h[:, 0].any():
+    print("halo units: start freed built | mma_start mma_issued")
+    for u in range(12):
+        print(u, [int(v - t0) if v else -1 for v in h[u, :5]])
