@@ -37,3 +37,9 @@ if h[:, 0].any():
     print("halo units: start freed built | mma_start mma_issued")
     for u in range(12):
         print(u, [int(v - t0) if v else -1 for v in h[u, :5]])
+c = t[3968:3968 + 128].reshape(16, 8)
+if c[:, 0].any():
+    print("epilogue warp 0 chunk phases (clk): ld->tt | tt->loop | loop | ->store | store->issue-done")
+    for k in range(12):
+        r = c[k]
+        print(k + 8, [int(r[1] - r[0]), int(r[3] - r[1]), int(r[4] - r[3]), int(r[5] - r[4]), int(r[6] - r[5])])
