@@ -102,6 +102,17 @@ def engine_peaks():
         return {}
 
 
+def measured_traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per image of the kernel behind layer key,
+    from the ncu capture summarized in profiles/traffic.json (None if absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(key)
+    except Exception:
+        return None
+
+
 def roofline(m, B, i, ms, engine):
     """Roofline of layer i from its measured device time: algorithmic work per launch
      / duration, against the measured peak of the bounding unit."""
@@ -333,6 +344,10 @@ def main():
     top = int(np.argmax(layer_ms))
     roof = roofline(m, B, top, layer_ms[top], engines[top])
     roof["share_of_step"] = float(layer_ms[top] / layer_ms.sum())
+    tr = measured_traffic(f"layer{top}:{engines[top]}")
+    if tr is not None:  # DRAM bytes per launch from the committed ncu capture, scaled to B
+        roof["traffic"] = tr["bytes_per_image"] * B
+        roof["traffic_source"] = tr["source"]
 
     out = None
     if rank == 0:

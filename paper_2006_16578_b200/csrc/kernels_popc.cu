@@ -579,18 +579,32 @@ void launch_or_pool(const uint64_t* in, int H, int W, size_t plane_words, int wi
   BT_CUDA(cudaGetLastError());
 }
 
+// One warp per row: each lane keeps the first maximum of its strided classes, then a
+// shuffle reduction keeps the larger value and, on ties, the smaller index — the same
+// first-index argmax as the sequential scan (inference.hpp:177-184; logits are finite).
 __global__ void argmax_kernel(const double* __restrict__ logits, int batch, int classes, int32_t* labels) {
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < batch; n += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int n = (blockIdx.x * blockDim.x + threadIdx.x) / 32; n < batch; n += gridDim.x * blockDim.x / 32) {
     const double* row = logits + (size_t)n * classes;
-    int best = 0;
-    for (int j = 1; j < classes; ++j)
-      if (row[j] > row[best]) best = j;
-    labels[n] = best;
+    double bv = lane < classes ? row[lane] : -INFINITY;
+    int bi = lane < classes ? lane : INT_MAX;
+    for (int j = lane + 32; j < classes; j += 32) {
+      const double v = row[j];
+      if (v > bv) { bv = v; bi = j; }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) labels[n] = bi;
   }
 }
 void launch_argmax(const double* logits, int batch, int classes, int32_t* labels, cudaStream_t st) {
   if (batch <= 0) return;
-  argmax_kernel<<<(batch + 127) / 128, 128, 0, st>>>(logits, batch, classes, labels);
+  const int blocks = (batch + 7) / 8;
+  argmax_kernel<<<blocks < 148 * 8 ? blocks : 148 * 8, 256, 0, st>>>(logits, batch, classes, labels);
   BT_CUDA(cudaGetLastError());
 }
 
