@@ -18,10 +18,16 @@ plan = btnn.Plan(m, ws, B)
 x = np.random.default_rng(2).standard_normal((B, 224, 224, 3), dtype=np.float32)
 plan.run(x)
 plan.run(x)
-ts = np.zeros(512, dtype=np.uint64)
-capi.check(capi.lib().btnn_cuda_debug_ftc_timestamps(ts.ctypes.data_as(C.POINTER(C.c_uint64)), 512))
-t = ts.astype(np.int64).reshape(64, 8)
+ts = np.zeros(640, dtype=np.uint64)
+capi.check(capi.lib().btnn_cuda_debug_ftc_timestamps(ts.ctypes.data_as(C.POINTER(C.c_uint64)), 640))
+t = ts[:512].astype(np.int64).reshape(64, 8)
 t0 = t[t > 0].min()
 print("tile: bstart bfree bdone | mma_start mma_issued | epi_start epi_done  (clk rel. to first stamp)")
 for i in range(40):
     print(i, (t[i, :7] - t0).tolist())
+
+e = ts[512:640].astype(np.int64).reshape(8, 16)
+print("epilogue warp 0 per group: [ld-wait, process, flush] (clk)")
+for i in range(8):
+    r = e[i]
+    print(i + 4, [[int(r[1 + 3 * g] - (r[0] if g == 0 else r[3 * g])), int(r[2 + 3 * g] - r[1 + 3 * g]), int(r[3 + 3 * g] - r[2 + 3 * g])] for g in range(4)])
