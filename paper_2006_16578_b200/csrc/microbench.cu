@@ -127,6 +127,49 @@ __global__ void __launch_bounds__(128, 1) tc_sw64_kernel(int iters, long long* c
   if (warp == 0) tmem_dealloc(tb, 512);
 }
 
+// SS-mode with moving operands, as in a real GEMM: A walks 8 distinct 128x64-byte
+// SWIZZLE_64B tiles (64 KB) and B 8 distinct Nx64-byte tiles, so no two consecutive MMAs read
+// the same shared-memory bytes.
+template <int N>
+__global__ void __launch_bounds__(128, 1) tc_sw64_moving_kernel(int iters, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* as = smem;                 // 8 x 128 x 64 bytes
+  uint8_t* bs = smem + 8 * 128 * 64;  // 8 x N x 64 bytes
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  for (int i = tid; i < 8 * (128 + N) * 64 / 16; i += 128) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x01010101u, 0, 0, 0);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tb = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(128, N);
+    const uint64_t ad = sdesc_sw(smem_u32(as), 64), bd = sdesc_sw(smem_u32(bs), 64);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t k = (uint32_t)((it * 4 + j) & 15);  // tile (k>>1), K half (k&1)
+        mma_i8_ss(tb, ad + (k >> 1) * (128 * 64 / 16) + 2 * (k & 1), bd + (k >> 1) * (N * 64 / 16) + 2 * (k & 1),
+                  id, 1);
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tb, 512);
+}
+
 // tcgen05 i8 throughput: one thread issues iters x 4 MMAs (M128 x N x K32) back to back.
 template <bool ATMEM, int N>
 __global__ void __launch_bounds__(128, 1) tc_peak_kernel(int iters, long long* cycles) {
@@ -331,6 +374,24 @@ int main() {
   tc(tc_peak_kernel<false, 64>, 64, false, "tc_i8_smemA_n64");
   tc(tc_sw64_kernel<64>, 64, false, "tc_i8_smemA_sw64_n64");
   tc(tc_sw64_kernel<128>, 128, false, "tc_i8_smemA_sw64_n128");
+  {
+    auto tcm = [&](auto kern, int N, const char* name) {
+      const int iters = 4096;
+      const size_t smem = 8 * (128 + N) * 64;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const float ms = time_ms([&] { kern<<<sms, 128, smem>>>(iters, d_cyc); });
+      std::vector<long long> cyc(sms);
+      cudaMemcpy(cyc.data(), d_cyc, sms * 8, cudaMemcpyDeviceToHost);
+      double mean = 0;
+      for (auto c : cyc) mean += c;
+      mean /= sms;
+      const double macs = (double)iters * 4 * 128 * N * 32 * sms;
+      printf(", \"%s\": {\"tmacs\": %.1f, \"mac_per_clk_sm\": %.0f, \"clk_per_mma\": %.1f, \"ms\": %.3f}", name,
+             macs / ms / 1e9, (double)iters * 4 * 128 * N * 32 / mean, mean / (iters * 4.0), ms);
+    };
+    tcm(tc_sw64_moving_kernel<64>, 64, "tc_i8_smemA_sw64_moving_n64");
+    tcm(tc_sw64_moving_kernel<128>, 128, "tc_i8_smemA_sw64_moving_n128");
+  }
 
   // ---- legacy warp MMA, popc, fp64: grid 148*8 blocks x 256 threads
   const int blocks = sms * 8, threads = 256, it = 2048;
