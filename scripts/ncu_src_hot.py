@@ -1,0 +1,55 @@
+"""Aggregate an `ncu --page source --csv --print-source cuda,sass` export by source line.
+
+Prints the hottest source lines (warp-stall samples) with their top stall reasons.
+  ncu -i rep --page source --csv --print-source cuda,sass --kernel-name regex:K \
+      --launch-skip S --launch-count 1 > src.csv; python scripts/ncu_src_hot.py src.csv [N]
+"""
+import csv
+import sys
+from collections import defaultdict
+
+
+def main():
+    path = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+    rows = list(csv.reader(open(path)))
+    fname, hdr, line, src = None, None, None, None
+    agg = defaultdict(lambda: defaultdict(float))
+    text = {}
+    for r in rows:
+        if not r:
+            continue
+        if r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+            continue
+        if r[0] == "Line No":
+            hdr = r
+            continue
+        if hdr is None or len(r) < len(hdr):
+            continue
+        if r[0]:
+            line, src = int(r[0]), r[1]
+            text[(fname, line)] = src.strip()
+            continue
+        if r[2] in ("-", "..."):
+            continue
+        key = (fname, line)
+        for i, h in enumerate(hdr):
+            if i < 4:
+                continue
+            if h == "Warp Stall Sampling (All Samples)" or (h.startswith("stall_") and "Not Issued" not in h):
+                try:
+                    agg[key][h] += float(r[i])
+                except ValueError:
+                    pass
+    tot = sum(v["Warp Stall Sampling (All Samples)"] for v in agg.values())
+    hot = sorted(agg.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:top]
+    for (f, ln), v in hot:
+        s = v["Warp Stall Sampling (All Samples)"]
+        reasons = sorted(((k[6:], x) for k, x in v.items() if k.startswith("stall_")), key=lambda t: -t[1])[:3]
+        rs = " ".join(f"{k}:{100 * x / max(s, 1):.0f}%" for k, x in reasons if x > 0)
+        print(f"{100 * s / tot:5.1f}% {f}:{ln:<5} {rs:40s} {text.get((f, ln), '')[:70]}")
+
+
+if __name__ == "__main__":
+    main()
