@@ -27,7 +27,8 @@ for i in range(40):
     print(i, (t[i, :7] - t0).tolist())
 
 e = ts[512:640].astype(np.int64).reshape(8, 16)
-print("epilogue warp 0 per group: [ld-wait, process, flush] (clk)")
+print("epilogue warp 0 per channel half: [acc wait, process, tap store] (clk)")
 for i in range(8):
     r = e[i]
-    print(i + 4, [[int(r[1 + 3 * g] - (r[0] if g == 0 else r[3 * g])), int(r[2 + 3 * g] - r[1 + 3 * g]), int(r[3 + 3 * g] - r[2 + 3 * g])] for g in range(4)])
+    print(i + 4, [[int(r[1 + 3 * h] - (r[0] if h == 0 else r[3 * h])), int(r[2 + 3 * h] - r[1 + 3 * h]),
+                   int(r[3 + 3 * h] - r[2 + 3 * h])] for h in range(2)])
