@@ -126,3 +126,28 @@ def test_halved_tap_equals_adapt_shortcut():
     want = (((a + b) + c) + d) * 0.25
     assert np.array_equal(half.view(np.uint64), want.view(np.uint64))
     assert np.array_equal(lg_half.view(np.uint64), lg_full.view(np.uint64))
+
+
+def test_signed_zero_taps_fire():
+    """bn-route outputs equal to -0.0 must fire (y >= 0.0 holds for -0.0, bconv.hpp:191):
+    gamma < 0 and beta = -0.0 turn every v == mean into y = -0.0 (x = +0, q = +0, q*gamma = -0,
+    -0 + -0 = -0), and a zero image makes that happen across whole first-layer tiles; the
+    residual add then sees -0.0 + -0.0. The epilogues read the sign off the f64 bit pattern on
+    channels with finite parameters (bnmath.cuh nonneg_bit), so this pins the -0.0 case."""
+    m = M.make_model("negzero", "16C7/4-16C3-16C3-16C3-8FC", 32, 32, 3, 8, [(0, 2), (2, 3)])
+    fw = Wt.random_weights(m, 41)
+    for li in (0, 2, 3):
+        lw = fw.layers[li]
+        ch = lw["gamma"].shape[0]
+        lw["gamma"] = -np.abs(lw["gamma"]) - 0.1
+        lw["gamma"][::4] *= -1.0  # some channels keep gamma > 0: +0 + -0 = +0
+        lw["beta"] = np.full(ch, -0.0)
+        lw["mean"] = np.zeros(ch)
+    ws = Wt.build_weights(m, fw)
+    x = np.random.default_rng(42).standard_normal((6, 32, 32, 3), dtype=np.float32)
+    x[0] = 0.0
+    x[3, :16] = 0.0
+    lg, lb = B.Plan(m, ws, 6).run(x)
+    want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+    assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(lb, wl)
