@@ -74,10 +74,10 @@ void launch_first_conv_signbits(const float* w_pm1, int O, int K, uint32_t* out,
 // Tensor-core first layer (kernels_first_tc.cu): exact integer-digit MMAs with a
 // sequential-f64 fix-up pass for windows whose terms do not fit the tile's grid.
 // Encode a 4-D f64 TMA tensor map (dims[0] contiguous; strides in bytes for dims 1..3;
-// SWIZZLE_128B boxes, out-of-range elements zero-filled on load and clipped on store).
+// SWIZZLE_128B or dense boxes, out-of-range elements zero-filled on load and clipped on store).
 // False when the driver entry point is missing or the layout is not TMA-compatible.
 bool encode_f64_map(CUtensorMap* m, const double* base, const uint64_t dims[4], const uint64_t strides[3],
-                    const uint32_t box[4]);
+                    const uint32_t box[4], bool swizzle128 = true);
 
 bool first_conv_tc_supported(const FirstConvArgs& a);
 size_t first_conv_tc_weight_bytes(int KH, int KW);
