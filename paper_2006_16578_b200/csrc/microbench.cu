@@ -170,6 +170,91 @@ __global__ void __launch_bounds__(128, 1) tc_sw64_moving_kernel(int iters, long 
   if (warp == 0) tmem_dealloc(tb, 512);
 }
 
+// The halo-mode MMA sequence of bgemm_tc_kernel (3x3 conv, C = 64, NI = 8 images x 16 sites):
+// per unit 9 taps x 2 K halves, A = 128 rows at row offset (r*18 + s)*8 of a SWIZZLE_64B
+// halo (multiples of 512 B), B = the tap's 64 x 64 block (4 KB apart), one accumulator.
+// ALIGN1K pads the halo so every tap starts on a 1024-byte boundary (row offsets * 2).
+template <int N, bool ALIGN1K, bool DENSE = false, bool TMEMLD = false, bool WARPWIDE = false>
+__global__ void __launch_bounds__(128, 1) tc_halo_pattern_kernel(int iters, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* as = smem;               // halo: up to 2 * 56 * 512 bytes
+  uint8_t* bs = smem + 56 * 1024;   // 9 x N x 64 bytes
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  for (int i = tid; i < (56 * 1024 + 9 * N * 64) / 16; i += 128) {
+    if (DENSE) {  // random +-1 bytes (0x01 / 0xFF), like expanded activations and weights
+      uint32_t w[4];
+      for (int k = 0; k < 4; ++k) {
+        uint32_t h = (uint32_t)(i * 4 + k) * 2654435761u;
+        h ^= h >> 15;
+        h *= 2246822519u;
+        h ^= h >> 13;
+        w[k] = 0x01010101u | ((h & 0x01010101u) * 0xFEu);
+      }
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x01010101u, 0, 0, 0);
+    }
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tb = tbase;
+  if (WARPWIDE && warp == 0) {  // the kernel's issue style: whole warp loops, elect.sync issues
+    const uint32_t id = idesc_i8(128, N);
+    const uint64_t ad = sdesc_sw(smem_u32(as), 64), bd = sdesc_sw(smem_u32(bs), 64);
+    uint32_t aoff[9];
+    for (int t = 0; t < 9; ++t) aoff[t] = (uint32_t)(((t / 3) * 18 + t % 3) * 8 * 64 / 16);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        mma_i8_ss_w(tb, ad + aoff[t], bd + t * (N * 64 / 16), id, 1);
+        mma_i8_ss_w(tb, ad + aoff[t] + 2, bd + t * (N * 64 / 16) + 2, id, 1);
+      }
+    }
+    mma_commit_w(&bar);
+    mbar_wait(&bar, 0);
+    if (tid == 0) cycles[blockIdx.x] = clock64() - t0;
+  } else if (!WARPWIDE && tid == 0) {
+    const uint32_t id = idesc_i8(128, N);
+    const uint64_t ad = sdesc_sw(smem_u32(as), 64), bd = sdesc_sw(smem_u32(bs), 64);
+    uint32_t aoff[9];
+    for (int t = 0; t < 9; ++t) aoff[t] = (uint32_t)(((t / 3) * 18 + t % 3) * 8 * 64 / 16) * (ALIGN1K ? 2 : 1);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        mma_i8_ss(tb, ad + aoff[t], bd + t * (N * 64 / 16), id, 1);
+        mma_i8_ss(tb, ad + aoff[t] + 2, bd + t * (N * 64 / 16) + 2, id, 1);
+      }
+    }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  } else if (TMEMLD && warp >= 1) {
+    // concurrent epilogue-like TMEM reads of another accumulator region (warps 1-3 read
+    // lane quarters 1-3; columns 256..)
+    uint32_t acc[32], sink = 0;
+    for (int it = 0; it < iters / 4; ++it) {
+      tmem_ld32(tb + ((uint32_t)(warp * 32) << 16) + 256 + (it & 7) * 32, acc);
+      tmem_ld_wait();
+      for (int j = 0; j < 32; ++j) sink += acc[j];
+    }
+    if (sink == 0x12345678u) cycles[0] = 0;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tb, 512);
+}
+
 // tcgen05 i8 throughput: one thread issues iters x 4 MMAs (M128 x N x K32) back to back.
 template <bool ATMEM, int N>
 __global__ void __launch_bounds__(128, 1) tc_peak_kernel(int iters, long long* cycles) {
@@ -391,6 +476,27 @@ int main() {
     };
     tcm(tc_sw64_moving_kernel<64>, 64, "tc_i8_smemA_sw64_moving_n64");
     tcm(tc_sw64_moving_kernel<128>, 128, "tc_i8_smemA_sw64_moving_n128");
+    auto tch = [&](auto kern, int N, const char* name) {
+      const int iters = 2048;
+      const size_t smem = 56 * 1024 + 9 * N * 64;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const float ms = time_ms([&] { kern<<<sms, 128, smem>>>(iters, d_cyc); });
+      std::vector<long long> cyc(sms);
+      cudaMemcpy(cyc.data(), d_cyc, sms * 8, cudaMemcpyDeviceToHost);
+      double mean = 0;
+      for (auto c : cyc) mean += c;
+      mean /= sms;
+      const double macs = (double)iters * 18 * 128 * N * 32 * sms;
+      printf(", \"%s\": {\"tmacs\": %.1f, \"clk_per_mma\": %.1f, \"ms\": %.3f}", name, macs / ms / 1e9,
+             mean / (iters * 18.0), ms);
+    };
+    tch(tc_halo_pattern_kernel<64, false>, 64, "tc_i8_halo_pattern_n64");
+    tch(tc_halo_pattern_kernel<64, true>, 64, "tc_i8_halo_pattern_n64_align1k");
+    tch(tc_halo_pattern_kernel<128, false>, 128, "tc_i8_halo_pattern_n128");
+    tch(tc_halo_pattern_kernel<64, false, true>, 64, "tc_i8_halo_pattern_n64_dense_pm1");
+    tch(tc_halo_pattern_kernel<64, false, true, true>, 64, "tc_i8_halo_pattern_n64_with_tmem_ld");
+    tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_warpwide_elect");
+    tch(tc_halo_pattern_kernel<128, false, true>, 128, "tc_i8_halo_pattern_n128_dense_pm1");
   }
 
   // ---- legacy warp MMA, popc, fp64: grid 148*8 blocks x 256 threads

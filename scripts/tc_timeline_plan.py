@@ -43,3 +43,10 @@ if c[:, 0].any():
     for k in range(12):
         r = c[k]
         print(k + 8, [int(r[1] - r[0]), int(r[3] - r[1]), int(r[4] - r[3]), int(r[5] - r[4]), int(r[6] - r[5])])
+m = t[1024:1024 + 512].reshape(16, 32)
+if m[:, 0].any() and not t[1024 + 16 * 32:1024 + 16 * 32 + 1].any():
+    print("halo MMA issue stamps per tap (clk since the unit's first tap):")
+    for u in range(8):
+        r = m[u]
+        if r[0]:
+            print(u, [int(v - r[0]) for v in r[:9]])
