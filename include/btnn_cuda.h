@@ -233,6 +233,22 @@ typedef struct {
 
 typedef struct btnn_plan btnn_plan;
 
+/* ---- file ingestion -------------------------------------------- */
+/* load_weights (weights.hpp:354-445): a BTNN bit-weight file for `model`, with the
+ * reference's checks (magic/version/tags -> BTNN_IO_ERROR; layer count, kinds, dims, word
+ * and threshold counts -> BTNN_VALIDATION_ERROR; BnParams::validate -> BTNN_INVALID_INPUT).
+ * The store keeps the file's layout (plain, or tiled 8x128); the first conv's +-1 floats
+ * are unpacked from its filter bits (detail::unpack_first_conv, weights.hpp:231-240). */
+typedef struct btnn_loaded_weights btnn_loaded_weights;
+int btnn_cuda_load_weights(const char* path, const btnn_model_spec* model, btnn_loaded_weights** out);
+/* View for btnn_cuda_plan_create; valid until btnn_cuda_free_weights. */
+int btnn_cuda_loaded_weights_store(const btnn_loaded_weights* w, btnn_weight_store* out);
+int btnn_cuda_free_weights(btnn_loaded_weights* w);
+/* read_batch (io.hpp:83-101): BTIN header -> n, h, w, c (whole samples only), then the
+ * f32 NHWC payload into out (capacity in floats). BTNN_IO_ERROR on a malformed file. */
+int btnn_cuda_batch_dims(const char* path, size_t* n, size_t* h, size_t* w, size_t* c);
+int btnn_cuda_read_batch(const char* path, float* out, size_t capacity);
+
 /* Build a device plan: validate model/weights like run_inference (inference.hpp:69-75),
  * convert weights to the device formats and upload them once to every listed device.
  * max_batch bounds the per-call batch; the batch is sharded across the devices in

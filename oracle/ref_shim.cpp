@@ -19,6 +19,7 @@
 #include "btnn/bit_matrix.hpp"
 #include "btnn/bmm.hpp"
 #include "btnn/inference.hpp"
+#include "btnn/io.hpp"
 #include "btnn/layer_math.hpp"
 #include "btnn/model.hpp"
 #include "btnn/oracle.hpp"
@@ -220,6 +221,32 @@ void* ref_build_weights(void* model, void* fwp, int tiled, size_t bh, size_t bw,
 }
 const btnn_weight_store* ref_store_view(void* ws) { return &static_cast<Store*>(ws)->view; }
 void ref_store_free(void* ws) { delete static_cast<Store*>(ws); }
+
+// ---- files: save_weights (weights.hpp:302-352), write_batch (io.hpp:71-80), and the
+// `btnn infer` flow load_weights + read_batch + run_inference (btnn_cli.cpp:69-110) ----
+int ref_save_weights(void* model, void* ws, const char* path) {
+  return guard([&] { btnn::save_weights(path, static_cast<Model*>(model)->m, static_cast<Store*>(ws)->ws); });
+}
+int ref_write_batch(const float* x, size_t n, size_t h, size_t w, size_t c, const char* path) {
+  return guard([&] {
+    btnn::RealTensorNHWC t(n, h, w, c);
+    std::memcpy(t.v.data(), x, t.v.size() * sizeof(float));
+    btnn::write_batch(path, t);
+  });
+}
+int ref_infer_files(void* model, const char* wpath, int tiled, const char* bpath, size_t max_batch, double* logits,
+                    int32_t* labels, size_t* n_out) {
+  auto& m = static_cast<Model*>(model)->m;
+  return guard([&] {
+    const btnn::WeightStore ws = btnn::load_weights(wpath, m, tiled != 0);
+    const btnn::RealTensorNHWC in = btnn::read_batch(bpath);
+    if (in.batch > max_batch) throw btnn::invalid_input("ref_infer_files: batch larger than the output buffers");
+    auto r = btnn::run_inference(m, ws, in, {});
+    std::memcpy(logits, r.logits.data(), r.logits.size() * sizeof(double));
+    for (size_t i = 0; i < r.labels.size(); ++i) labels[i] = r.labels[i];
+    *n_out = in.batch;
+  });
+}
 
 // ---- inputs: the CLI's seeded N(0,1) floats (btnn_cli.cpp:76-79) ----
 void ref_normal_floats(uint64_t seed, float* out, size_t n) {

@@ -187,13 +187,47 @@ def convert_activations(d: capi.ActDesc, words, tiled, bh=8, bw=128):
 
 
 # ---- model driver (inference.hpp:67-186) ---------------------------------------------
+class LoadedWeights:
+    """load_weights (weights.hpp:354-445) of a BTNN bit-weight file, parsed by the library
+    (btnn_cuda_load_weights) with the reference's checks; pass it to Plan like a store."""
+
+    def __init__(self, path: str, m):
+        self._spec = m.c_spec() if isinstance(m, Model) else m
+        h = C.c_void_p()
+        check(lib().btnn_cuda_load_weights(str(path).encode(), C.byref(self._spec), C.byref(h)))
+        self.h = h
+
+    def c_store(self):
+        st = capi.WeightStore()
+        check(lib().btnn_cuda_loaded_weights_store(self.h, C.byref(st)))
+        return st
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().btnn_cuda_free_weights(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def read_batch(path: str) -> np.ndarray:
+    """read_batch (io.hpp:83-101): a BTIN file as an (n, h, w, c) float32 array."""
+    n, h, w, c = C.c_size_t(), C.c_size_t(), C.c_size_t(), C.c_size_t()
+    p = str(path).encode()
+    check(lib().btnn_cuda_batch_dims(p, C.byref(n), C.byref(h), C.byref(w), C.byref(c)))
+    x = np.empty((n.value, h.value, w.value, c.value), dtype=np.float32)
+    check(lib().btnn_cuda_read_batch(p, _p(x, C.c_float), x.size))
+    return x
+
+
 class Plan:
     """A device plan for (model, weight store); run() is run_inference on host arrays."""
 
     def __init__(self, m: Model, ws, max_batch: int, devices=(0,)):
         self.model = m
         self._spec = m.c_spec() if isinstance(m, Model) else m
-        self._store = ws.c_store() if isinstance(ws, WeightStoreHost) else ws
+        self._store = ws.c_store() if hasattr(ws, "c_store") else ws
         devs = (C.c_int * len(devices))(*devices)
         h = C.c_void_p()
         check(lib().btnn_cuda_plan_create(C.byref(self._spec), C.byref(self._store), max_batch, devs, len(devices),

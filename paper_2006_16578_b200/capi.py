@@ -126,6 +126,11 @@ _PROTOS = {
     "btnn_cuda_debug_ftc_timestamps": (C.c_int, [P(C.c_uint64), sz]),
     "btnn_cuda_plan_layer_engine": (C.c_char_p, [C.c_void_p, sz]),
     "btnn_cuda_plan_destroy": (C.c_int, [C.c_void_p]),
+    "btnn_cuda_load_weights": (C.c_int, [C.c_char_p, P(ModelSpec), P(C.c_void_p)]),
+    "btnn_cuda_loaded_weights_store": (C.c_int, [C.c_void_p, P(WeightStore)]),
+    "btnn_cuda_free_weights": (C.c_int, [C.c_void_p]),
+    "btnn_cuda_batch_dims": (C.c_int, [C.c_char_p, P(sz), P(sz), P(sz), P(sz)]),
+    "btnn_cuda_read_batch": (C.c_int, [C.c_char_p, f32p, sz]),
 }
 
 EXPORTS = tuple(_PROTOS)

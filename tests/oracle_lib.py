@@ -87,6 +87,9 @@ _REF = {
     "ref_fold_bn_sign": (None, [C.c_double] * 5 + [f64p, u8p]),
     "ref_bn_apply": (C.c_double, [BN, sz, C.c_double]),
     "ref_run_store": (C.c_int, [P(capi.ModelSpec), P(capi.WeightStore), f32p, sz, f64p, i32p]),
+    "ref_save_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_char_p]),
+    "ref_write_batch": (C.c_int, [f32p, sz, sz, sz, sz, C.c_char_p]),
+    "ref_infer_files": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int, C.c_char_p, sz, f64p, i32p, P(sz)]),
 }
 
 _oracle = None
