@@ -70,6 +70,6 @@ bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter*
 // Tensor-core support (kernels_tc.cu).
 bool tc_supported(const ConvShape& s, const Epi& e);
 void tc_prepare_filter(const ConvShape& s, const uint64_t* filt_plain, TcFilter& out, cudaStream_t st);
-void launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st);
+bool launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st);
 
 }  // namespace btnn_gpu

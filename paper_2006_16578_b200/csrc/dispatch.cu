@@ -39,8 +39,7 @@ const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t
   require(e.rout_half == nullptr || (tc_ok && h != EngineHint::Popc), BTNN_CUDA_ERROR,
           "halved tap output needs the tensor-core engine");
   if (tc_ok && h != EngineHint::Popc) {
-    launch_bgemm_tc(s, act, *tc, e, st);
-    return "tc_i8";
+    return launch_bgemm_tc(s, act, *tc, e, st) ? "tc_i8_splitk" : "tc_i8";
   }
   launch_bgemm_popc(s, act, filt, e, st);
   return "popc";

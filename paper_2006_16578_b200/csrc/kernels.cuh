@@ -29,7 +29,7 @@ struct ConvShape {
 };
 
 // Fused epilogue (bconv.hpp:160-194, bmm.hpp:219-274, inference.hpp:107-118/161-164).
-enum EpiMode { EPI_I32 = 0, EPI_BITS = 1, EPI_F64 = 2 };
+enum EpiMode { EPI_I32 = 0, EPI_BITS = 1, EPI_F64 = 2, EPI_SPLIT = 3 /* tensor-core split-K partial sums (internal) */ };
 struct Epi {
   int mode = EPI_I32;
   int raw = 0;                       // EPI_I32: write the raw xor-popcount (bmm_raw)
@@ -45,6 +45,8 @@ struct Epi {
   const double* rin = nullptr;       // residual_in, PQNO over (rin_P, rin_Q, N, rin_C)
   int rin_P = 0, rin_Q = 0, rin_C = 0, rin_halve = 0;  // type-A adaptation (inference.hpp:43-63)
   double* rout = nullptr;            // residual_out / logits, PQNO over (P, Q, N, O)
+  int32_t* split_ws = nullptr;       // optional zeroed-by-callee int32 M x O workspace: lets the
+                                     //   tensor-core engine split few-tile FC GEMMs along K
   double* rout_half = nullptr;       // residual_out pre-averaged for a halving consumer,
                                      //   PQNO over (P/2, Q/2, N, O) (tensor-core engine only)
 };

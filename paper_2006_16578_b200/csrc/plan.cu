@@ -39,6 +39,7 @@ struct LayerDev {
   bool has_thr = false, has_bn = false;
   DevBuf tap;           // residual_out, PQNO f64 sized for max batch
   DevBuf tap_half;      // residual_out pre-averaged 2x2 for a halving consumer (P/2, Q/2, N, O)
+  DevBuf split_ws;      // fc layers: int32 batch x units workspace for split-K (tensor-core engine)
   bool feeds_full = false, feeds_half = false;  // consumers read the tap as is / halved
   bool wrote_half = false;                      // last enqueue stored tap_half instead of tap
   bool halo_ok = false;                         // conv may run the halo-mode kernel (filter layout)
@@ -173,6 +174,7 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
     if (l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC) {
       fc_max = std::max(fc_max, B * ru(l.in_channels, 128) / 64);
       fc_max = std::max(fc_max, B * ru(l.units, 128) / 64);
+      L.split_ws.alloc(B * l.units * sizeof(int32_t));
     }
     if (l.kind == BTNN_FIRST_CONV_BWN) {
       L.wpm1 = upload(w.conv_pm1, w.conv_pm1_n, st);
@@ -401,6 +403,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         e.out_bits = out;
         e.thr_lo = L.thr_lo.get<long long>();
         e.thr_hi = L.thr_hi.get<long long>();
+        e.split_ws = L.split_ws.get<int32_t>();
         L.engine = launch_bgemm(s, sh.fc[fcur].get<uint64_t>(), L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
         fcur ^= 1;
       } else {
@@ -409,9 +412,10 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         e.bn_mean = L.bn.get<double>(); e.bn_s = e.bn_mean + O; e.bn_gamma = e.bn_mean + 2 * O; e.bn_beta = e.bn_mean + 3 * O;
         e.bn_rcp = e.bn_mean + 4 * O;
         e.rout = d_logits;  // logits = bn(v) (inference.hpp:161-164)
+        e.split_ws = L.split_ws.get<int32_t>();
         L.engine = launch_bgemm(s, sh.fc[fcur].get<uint64_t>(), L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
       }
-      ++launches;
+      launches += L.engine == std::string("tc_i8_splitk") ? 2 : 1;
     }
   }
   if (timed) BT_CUDA(cudaEventRecord(sh.events[sh.layers.size()], st));
