@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <string>
@@ -24,7 +25,7 @@
 
 namespace btnn_gpu {
 
-constexpr size_t kChunk = 128, kMaxChunks = 8;  // run_shard_host's input pipelining
+constexpr size_t kChunk = 64, kMaxChunks = 8;  // run_shard_host input pipelining (BTNN_E2E_CHUNK overrides)
 
 struct LayerDev {
   btnn_layer_spec spec{};
@@ -465,7 +466,12 @@ static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t ba
   BT_CUDA(cudaSetDevice(sh.device));
   const size_t xin = plan->in_h * plan->in_w * plan->in_c;
   const bool timed = plan->breakdown && &sh == plan->shards[0].get();
-  const size_t nch = timed ? 1 : std::max<size_t>(1, std::min(kMaxChunks, batch / kChunk));
+  static const size_t chunk = [] {
+    const char* v = std::getenv("BTNN_E2E_CHUNK");
+    const long c = v ? std::atol(v) : 0;
+    return c > 0 ? (size_t)c : kChunk;
+  }();
+  const size_t nch = timed ? 1 : std::max<size_t>(1, std::min(kMaxChunks, batch / chunk));
   const size_t per = cdiv(batch, nch);
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
   for (size_t k = 0; k < nch; ++k) {
