@@ -188,9 +188,10 @@ def kernel_suites(reps=10, warmup=3):
 
 
 # ------------------------------------------------------------------ CPU reference arm
-def cpu_reference(model_name: str, seconds: float, seed: int = 1):
-    """Times the reference's own run_inference (oracle/_ref, all host threads) on a
-    bounded sample of the workload; returns (img/s, cores, sample description)."""
+def cpu_reference(model_name: str, seconds: float, seed: int = 1, steps: int = 3, warmup: int = 0):
+    """Times the reference's own run_inference (oracle/_ref, all host threads): `warmup`
+    untimed and `steps` timed steps, each a bounded sample of the workload sized so the
+    timed steps take about `seconds` in total; returns (img/s, cores, sample description)."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import ctypes as C
 
@@ -219,12 +220,16 @@ def cpu_reference(model_name: str, seconds: float, seed: int = 1):
         assert st == 0, r.ref_last_error()
         return dt
 
-    t1 = run(min(cores, 8))  # warm-up + rate estimate
+    t1 = run(min(cores, 8))  # rate estimate
     rate = min(cores, 8) / t1
-    nimg = max(cores, int(rate * seconds / 3))
-    times = [run(nimg) for _ in range(3)]
-    med = float(np.median(times))
-    return nimg / med, cores, f"{model_name} 224x224, {nimg} images/run, median of 3 runs, libbtnn_ref_{ref_variant()}"
+    steps = max(1, steps)
+    nimg = max(cores, int(rate * seconds / steps))
+    for _ in range(warmup):
+        run(nimg)
+    times = [run(nimg) for _ in range(steps)]
+    return (nimg * steps / float(sum(times)), cores,
+            f"{model_name} 224x224, {nimg} images per step, {steps} timed steps after {warmup} warm-up, "
+            f"libbtnn_ref_{ref_variant()}")
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -243,16 +248,18 @@ def main():
     if a.impl == "reference":
         if rank != 0:
             return
-        res = cpu_reference(a.model, a.cpu_seconds)
+        # the whole --steps K --warmup W run stays within a few minutes: ~1.5x cpu_seconds
+        res = cpu_reference(a.model, a.cpu_seconds, steps=a.steps, warmup=a.warmup)
         if res is None:
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
             return
         v, cores, sample = res
         print(json.dumps({"metric": f"{a.model} images/s (ImageNet 224x224, BNN inference)", "value": v,
-                          "unit": "images/s", "n_gpus": a.gpus, "steps": 3, "warmup": 1, "ms_per_step": None,
+                          "unit": "images/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+                          "ms_per_step": None,
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u1/f64",
                           "data": "synthetic", "impl": "reference",
-                          "config": {"workload": f"{a.model} 224x224x3 forward, reference CPU run_inference",
+                          "config": {"workload": f"{a.model} 224x224x3 forward (BNN, reference CPU run_inference)",
                                      "global_batch": None},
                           "cpu_baseline": {"value": v, "unit": "images/s", "cores": cores, "kind": "reference",
                                            "sample": sample},
