@@ -476,9 +476,9 @@ int main() {
     };
     tcm(tc_sw64_moving_kernel<64>, 64, "tc_i8_smemA_sw64_moving_n64");
     tcm(tc_sw64_moving_kernel<128>, 128, "tc_i8_smemA_sw64_moving_n128");
-    auto tch = [&](auto kern, int N, const char* name) {
+    auto tch = [&](auto kern, int N, const char* name, size_t smem_total = 0) {
       const int iters = 2048;
-      const size_t smem = 56 * 1024 + 9 * N * 64;
+      const size_t smem = smem_total ? smem_total : 56 * 1024 + 9 * N * 64;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const float ms = time_ms([&] { kern<<<sms, 128, smem>>>(iters, d_cyc); });
       std::vector<long long> cyc(sms);
@@ -496,6 +496,8 @@ int main() {
     tch(tc_halo_pattern_kernel<64, false, true>, 64, "tc_i8_halo_pattern_n64_dense_pm1");
     tch(tc_halo_pattern_kernel<64, false, true, true>, 64, "tc_i8_halo_pattern_n64_with_tmem_ld");
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_warpwide_elect");
+    tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_smem200k", 200 * 1024);
+    tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_smem225k", 225 * 1024);
     tch(tc_halo_pattern_kernel<128, false, true>, 128, "tc_i8_halo_pattern_n128_dense_pm1");
   }
 
