@@ -174,12 +174,12 @@ __global__ void __launch_bounds__(128, 1) tc_sw64_moving_kernel(int iters, long 
 // per unit 9 taps x 2 K halves, A = 128 rows at row offset (r*18 + s)*8 of a SWIZZLE_64B
 // halo (multiples of 512 B), B = the tap's 64 x 64 block (4 KB apart), one accumulator.
 // ALIGN1K pads the halo so every tap starts on a 1024-byte boundary (row offsets * 2).
-template <int N, bool ALIGN1K, bool DENSE = false, bool TMEMLD = false, bool WARPWIDE = false>
+template <int N, bool ALIGN1K, bool DENSE = false, bool TMEMLD = false, bool WARPWIDE = false, int COMMITS = 0>
 __global__ void __launch_bounds__(128, 1) tc_halo_pattern_kernel(int iters, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* as = smem;               // halo: up to 2 * 56 * 512 bytes
   uint8_t* bs = smem + 56 * 1024;   // 9 x N x 64 bytes
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid / 32;
   if (warp == 0) tmem_alloc(&tbase, 512);
@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(128, 1) tc_halo_pattern_kernel(int iters, long
   }
   if (tid == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&bar2, 1);
     fence_mbar_init();
   }
   fence_before();
@@ -218,6 +219,8 @@ __global__ void __launch_bounds__(128, 1) tc_halo_pattern_kernel(int iters, long
         mma_i8_ss_w(tb, ad + aoff[t], bd + t * (N * 64 / 16), id, 1);
         mma_i8_ss_w(tb, ad + aoff[t] + 2, bd + t * (N * 64 / 16) + 2, id, 1);
       }
+      // the kernel's per-unit commits (halo buffer free, accumulator full), never waited on here
+      for (int c = 0; c < COMMITS; ++c) mma_commit_w(&bar2);
     }
     mma_commit_w(&bar);
     mbar_wait(&bar, 0);
@@ -496,6 +499,7 @@ int main() {
     tch(tc_halo_pattern_kernel<64, false, true>, 64, "tc_i8_halo_pattern_n64_dense_pm1");
     tch(tc_halo_pattern_kernel<64, false, true, true>, 64, "tc_i8_halo_pattern_n64_with_tmem_ld");
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_warpwide_elect");
+    tch(tc_halo_pattern_kernel<64, false, true, false, true, 2>, 64, "tc_i8_halo_pattern_n64_2commits_per_unit");
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_smem200k", 200 * 1024);
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_smem225k", 225 * 1024);
     tch(tc_halo_pattern_kernel<128, false, true>, 128, "tc_i8_halo_pattern_n128_dense_pm1");
