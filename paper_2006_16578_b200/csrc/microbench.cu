@@ -174,8 +174,9 @@ __global__ void __launch_bounds__(128, 1) tc_sw64_moving_kernel(int iters, long 
 // per unit 9 taps x 2 K halves, A = 128 rows at row offset (r*18 + s)*8 of a SWIZZLE_64B
 // halo (multiples of 512 B), B = the tap's 64 x 64 block (4 KB apart), one accumulator.
 // ALIGN1K pads the halo so every tap starts on a 1024-byte boundary (row offsets * 2).
-template <int N, bool ALIGN1K, bool DENSE = false, bool TMEMLD = false, bool WARPWIDE = false, int COMMITS = 0>
-__global__ void __launch_bounds__(128, 1) tc_halo_pattern_kernel(int iters, long long* cycles) {
+template <int N, bool ALIGN1K, bool DENSE = false, bool TMEMLD = false, bool WARPWIDE = false, int COMMITS = 0,
+          bool POLLERS = false>
+__global__ void __launch_bounds__(576, 1) tc_halo_pattern_kernel(int iters, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* as = smem;               // halo: up to 2 * 56 * 512 bytes
   uint8_t* bs = smem + 56 * 1024;   // 9 x N x 64 bytes
@@ -241,6 +242,8 @@ __global__ void __launch_bounds__(128, 1) tc_halo_pattern_kernel(int iters, long
     mma_commit(&bar);
     mbar_wait(&bar, 0);
     cycles[blockIdx.x] = clock64() - t0;
+  } else if (POLLERS && warp >= 1) {  // the kernel's waiting roles: poll an mbarrier meanwhile
+    mbar_wait(&bar, 0);
   } else if (TMEMLD && warp >= 1) {
     // concurrent epilogue-like TMEM reads of another accumulator region (warps 1-3 read
     // lane quarters 1-3; columns 256..)
@@ -479,11 +482,11 @@ int main() {
     };
     tcm(tc_sw64_moving_kernel<64>, 64, "tc_i8_smemA_sw64_moving_n64");
     tcm(tc_sw64_moving_kernel<128>, 128, "tc_i8_smemA_sw64_moving_n128");
-    auto tch = [&](auto kern, int N, const char* name, size_t smem_total = 0) {
+    auto tch = [&](auto kern, int N, const char* name, size_t smem_total = 0, int threads = 128) {
       const int iters = 2048;
       const size_t smem = smem_total ? smem_total : 56 * 1024 + 9 * N * 64;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      const float ms = time_ms([&] { kern<<<sms, 128, smem>>>(iters, d_cyc); });
+      const float ms = time_ms([&] { kern<<<sms, threads, smem>>>(iters, d_cyc); });
       std::vector<long long> cyc(sms);
       cudaMemcpy(cyc.data(), d_cyc, sms * 8, cudaMemcpyDeviceToHost);
       double mean = 0;
@@ -500,6 +503,8 @@ int main() {
     tch(tc_halo_pattern_kernel<64, false, true, true>, 64, "tc_i8_halo_pattern_n64_with_tmem_ld");
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_warpwide_elect");
     tch(tc_halo_pattern_kernel<64, false, true, false, true, 2>, 64, "tc_i8_halo_pattern_n64_2commits_per_unit");
+    tch(tc_halo_pattern_kernel<64, false, true, false, true, 2, true>, 64, "tc_i8_halo_pattern_n64_17_polling_warps",
+        0, 576);
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_smem200k", 200 * 1024);
     tch(tc_halo_pattern_kernel<64, false, true, false, true>, 64, "tc_i8_halo_pattern_n64_smem225k", 225 * 1024);
     tch(tc_halo_pattern_kernel<128, false, true>, 128, "tc_i8_halo_pattern_n128_dense_pm1");
