@@ -325,7 +325,6 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     } else if (l.kind == BTNN_BIT_CONV) {
       const uint64_t* in = sh.act[cur].get<uint64_t>();
       uint64_t* out = sh.act[cur ^ 1].get<uint64_t>();
-      BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
       const ConvShape s = conv_shape(l, batch, L.halo_ok);
       Epi e;
       e.mode = EPI_BITS;
@@ -366,6 +365,10 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
           }
         }
       }
+      // The packed output is cleared first unless the tensor-core epilogue writes every word
+      // of it: no channel padding (O a multiple of 128) and no image padding (N a multiple of 8).
+      if (!(will_use_tc(s, e, EngineHint::Auto, &L.tc) && l.out_channels % 128 == 0 && np == batch))
+        BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
       L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
       ++launches;
       cur ^= 1;
