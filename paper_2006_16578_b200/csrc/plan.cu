@@ -296,7 +296,9 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     if (timed) BT_CUDA(cudaEventRecord(sh.events[i], st));
     if (l.kind == BTNN_FIRST_CONV_BWN) {
       uint64_t* out = sh.act[cur].get<uint64_t>();
-      BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
+      // the tensor-core kernel writes every word of its packed output when N % 8 == 0
+      if (!(first_tc && np == batch))
+        BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
       FirstConvArgs a{};
       a.x = d_x;
       a.w_pm1 = L.wpm1.get<float>();
@@ -365,9 +367,9 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
           }
         }
       }
-      // The packed output is cleared first unless the tensor-core epilogue writes every word
-      // of it: no channel padding (O a multiple of 128) and no image padding (N a multiple of 8).
-      if (!(will_use_tc(s, e, EngineHint::Auto, &L.tc) && l.out_channels % 128 == 0 && np == batch))
+      // The packed output is cleared first unless the tensor-core epilogue writes every word of
+      // it (channel-pad words included): no image padding (N a multiple of 8).
+      if (!(will_use_tc(s, e, EngineHint::Auto, &L.tc) && np == batch))
         BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
       L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
       ++launches;

@@ -70,7 +70,7 @@ def test_residual_variants_vs_oracle(tokens, hw, shortcuts):
     assert np.array_equal(lb, wl)
 
 
-@pytest.mark.parametrize("name,hw,batch", [("resnet18", 224, 2), ("alexnet", 224, 2), ("cifar-vgg", 32, 8),
+@pytest.mark.parametrize("name,hw,batch", [("resnet18", 224, 2), ("resnet18", 224, 8), ("alexnet", 224, 2), ("cifar-vgg", 32, 8),
                                             ("mnist-mlp", 28, 64), ("cifar-resnet14", 32, 8), ("vgg16", 64, 2)])
 def test_stock_models_vs_oracle(name, hw, batch):
     """The stock models (numpy-drawn weights) vs the C oracle; ResNet-18/AlexNet at full
@@ -151,3 +151,20 @@ def test_signed_zero_taps_fire():
     want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
     assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
     assert np.array_equal(lb, wl)
+
+
+@pytest.mark.parametrize("batch", [8, 16, 13])
+def test_uncleared_outputs_pad_words(batch):
+    """With N % 8 == 0 the plan does not clear packed outputs before tensor-core layers; the
+    epilogues write the channel-pad words themselves (O = 48 / 40 / 72 leave pad words in the
+    128-bit rows, including the tensor-core first conv). Stale bits from the previous use of
+    the ping-pong buffers must not leak: a second run on different inputs must match too."""
+    m = M.make_model("padw", "48C7/4-40C3-72C3-40C3-24FC", 64, 64, 3, 9, [(1, 3)])
+    ws = Wt.build_weights(m, Wt.random_weights(m, 51))
+    plan = B.Plan(m, ws, batch)
+    for seed in (52, 53):
+        x = np.random.default_rng(seed).standard_normal((batch, 64, 64, 3), dtype=np.float32)
+        lg, lb = plan.run(x)
+        want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+        assert np.array_equal(lg.view(np.uint64), want.view(np.uint64)), plan.engines()
+        assert np.array_equal(lb, wl)
