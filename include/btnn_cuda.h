@@ -166,11 +166,19 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
 int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t window,
                       size_t stride, uint64_t* out_words);
 
-/* Timing experiments only: copies the per-K-step clock64 stamps recorded by CTA 0 of the
- * last tensor-core GEMM launched with BTNN_TC_DBG & 16 (n <= 4096 entries). */
+/* Describes the last tensor-core bit GEMM launched from this host thread (kernel-level
+ * calls, or plans while their graph is captured): the kernel variant ("halo" or "tmemA",
+ * then "/thr", "/bn", "/i32" or "/split", plus "/pg2", "/blocked", "/bres" when they apply),
+ * the number of (tile, K-split) work units and the persistent grid size. Tests use it to
+ * prove which kernel path and how many tiles per CTA a case exercised. */
+int btnn_cuda_last_tc_launch(char* variant, size_t n, int* units, int* grid);
+
+/* Timing experiments only (builds with -DBTNN_TIMING=1): copies the per-K-step clock64
+ * stamps recorded by CTA 0 of the last tensor-core GEMM launched with BTNN_TC_DBG & 16
+ * (n <= 4096 entries). */
 int btnn_cuda_debug_tc_timestamps(unsigned long long* out, size_t n);
 
-/* Timing experiments only: per-tile clock64 stamps of CTA 0 of the last tensor-core first
+/* Timing experiments only (BTNN_TIMING builds): per-tile clock64 stamps of CTA 0 of the last tensor-core first
  * layer launched with BTNN_FTC_DBG=1 (n <= 512 entries, 8 per tile). */
 int btnn_cuda_debug_ftc_timestamps(unsigned long long* out, size_t n);
 
@@ -179,17 +187,31 @@ int btnn_cuda_debug_ftc_timestamps(unsigned long long* out, size_t n);
 int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* fast, double* ref);
 
 /* ---- benchmark suites (bench.hpp:129-299), device-timed ---------------------------- */
-/* bench_bmm: n x n x n; bin = 0 -> "bmm" (binarize float operands + bmm_pm1, int32 out),
- * bin = 1 -> "bmm-bin" (packed operands, bmm_pm1_bin sign rule). Random device operands;
- * median/min of `reps` CUDA-event-timed repetitions after `warmup`. `engine` receives the
- * engine name. Throughput = 2n^3 / median (bench.hpp:207-209). */
+/* Optional readback of a suite run, for the reference-style precheck (bench.hpp:164-176,
+ * 248-256): after timing, the device operands and the last result are copied to these host
+ * buffers (any may be NULL). bmm: a = n x n RowPacked A words, b = ColPacked B words,
+ * out = int32 n x n (bmm) or RowPacked bits (bmm-bin). bconv: a = packed HWNC input words,
+ * b = plain KKOC filter words, out = int32 PQNO (bconv) or HWNC bits (bconv-bin).
+ * kernel_ns (bmm only) receives the median of the GEMM alone with B already expanded. */
+typedef struct {
+  uint64_t* a_words;
+  uint64_t* b_words;
+  void* out;
+  double* kernel_ns;
+} btnn_bench_readback;
+/* bench_bmm: n x n x n on random packed +-1 words (bench.hpp:76-87, 136-137); bin = 0 ->
+ * "bmm" (bmm_pm1, int32 out), bin = 1 -> "bmm-bin" (bmm_pm1_bin sign rule, bit output).
+ * Every repetition is the whole call from packed operands (B's tensor-core expansion
+ * included). Median/min of `reps` CUDA-event-timed repetitions after `warmup`. `engine`
+ * receives the engine name. Throughput = 2n^3 / median (bench.hpp:207-209). */
 int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
-                        size_t engine_len);
+                        size_t engine_len, const btnn_bench_readback* rb);
 /* bench_bconv: input_hw x input_hw x batch x c -> o, k x k kernel, stride 1, pad k/2;
  * bin = 0 -> "bconv" (binarize + bconv_pm1), bin = 1 -> "bconv-bin" (bconv_fused with sign
  * thresholds, bench.hpp:238). Throughput = 2*P*Q*N*C*O*K^2 / median (bench.hpp:290-292). */
 int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
-                          double* median_ns, double* min_ns, char* engine, size_t engine_len);
+                          double* median_ns, double* min_ns, char* engine, size_t engine_len,
+                          const btnn_bench_readback* rb);
 
 /* ---- model driver (inference.hpp:67-186) ----------------------------------------- */
 /* LayerSpec (model.hpp:36-52), already resolved (resolve_model, model.hpp:190-296). */

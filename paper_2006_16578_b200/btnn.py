@@ -235,9 +235,14 @@ class Plan:
         self.h = h
         self.classes = self._spec.classes
         self.n_layers = self._spec.n_layers
+        self.in_dims = (self._spec.in_h, self._spec.in_w, self._spec.in_c)
 
     def run(self, x: np.ndarray):
         x = np.ascontiguousarray(x, dtype=np.float32)
+        # btnn_cuda_plan_run reads batch * in_h * in_w * in_c floats: the shape is checked
+        # here, as run_inference does (inference.hpp:69-75)
+        if x.ndim != 4 or tuple(x.shape[1:]) != self.in_dims:
+            raise capi.BtnnError(capi.BTNN_INVALID_INPUT, "run_inference: input dims do not match model")
         b = x.shape[0]
         logits = np.zeros(b * self.classes, dtype=np.float64)
         labels = np.zeros(b, dtype=np.int32)

@@ -53,6 +53,11 @@ class ConvFused(C.Structure):
                 ("threads", C.c_int)]
 
 
+class BenchReadback(C.Structure):
+    _fields_ = [("a_words", C.POINTER(C.c_uint64)), ("b_words", C.POINTER(C.c_uint64)), ("out", C.c_void_p),
+                ("kernel_ns", C.POINTER(C.c_double))]
+
+
 class LayerSpec(C.Structure):
     _fields_ = [("kind", C.c_int), ("kh", sz), ("kw", sz), ("out_channels", sz), ("stride", sz), ("pad", sz),
                 ("window", sz), ("pool_stride", sz), ("units", sz), ("in_h", sz), ("in_w", sz), ("in_channels", sz),
@@ -111,8 +116,9 @@ _PROTOS = {
     "btnn_cuda_bconv_fused": (C.c_int, [P(ActDesc), u64p, P(FilterDesc), u64p, P(ConvGeom), P(ConvFused), u64p]),
     "btnn_cuda_first_conv_bwn": (C.c_int, [f32p, sz, sz, sz, sz, f32p, sz, sz, sz, sz, P(ConvGeom), f64p]),
     "btnn_cuda_or_pool": (C.c_int, [P(ActDesc), u64p, sz, sz, u64p]),
-    "btnn_cuda_bench_bmm": (C.c_int, [sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz]),
-    "btnn_cuda_bench_bconv": (C.c_int, [sz, sz, sz, sz, sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz]),
+    "btnn_cuda_bench_bmm": (C.c_int, [sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz, P(BenchReadback)]),
+    "btnn_cuda_bench_bconv": (C.c_int, [sz, sz, sz, sz, sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz,
+                                        P(BenchReadback)]),
     "btnn_cuda_plan_create": (C.c_int, [P(ModelSpec), P(WeightStore), sz, P(C.c_int), C.c_int, P(C.c_void_p)]),
     "btnn_cuda_plan_run": (C.c_int, [C.c_void_p, f32p, sz, f64p, i32p]),
     "btnn_cuda_plan_run_device": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, sz, C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -123,6 +129,7 @@ _PROTOS = {
     "btnn_cuda_plan_tap_dims": (C.c_int, [C.c_void_p, sz, P(sz)]),
     "btnn_cuda_selftest_div": (C.c_int, [f64p, f64p, sz, f64p, f64p]),
     "btnn_cuda_debug_tc_timestamps": (C.c_int, [P(C.c_uint64), sz]),
+    "btnn_cuda_last_tc_launch": (C.c_int, [C.c_char_p, sz, P(C.c_int), P(C.c_int)]),
     "btnn_cuda_debug_ftc_timestamps": (C.c_int, [P(C.c_uint64), sz]),
     "btnn_cuda_plan_layer_engine": (C.c_char_p, [C.c_void_p, sz]),
     "btnn_cuda_plan_destroy": (C.c_int, [C.c_void_p]),
@@ -153,6 +160,14 @@ def lib() -> C.CDLL:
 def check(status: int) -> None:
     if status != BTNN_OK:
         raise BtnnError(status, lib().btnn_cuda_last_error().decode())
+
+
+def last_tc_launch():
+    """(variant, work units, grid) of the last tensor-core GEMM launched on this thread."""
+    buf = C.create_string_buffer(64)
+    units, grid = C.c_int(), C.c_int()
+    check(lib().btnn_cuda_last_tc_launch(buf, 64, C.byref(units), C.byref(grid)))
+    return buf.value.decode(), units.value, grid.value
 
 
 def set_engine(engine: int) -> None:

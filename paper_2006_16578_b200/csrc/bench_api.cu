@@ -2,7 +2,7 @@
 // (bench.hpp:129-299): bmm / bmm-bin over n x n x n, bconv / bconv-bin over
 // input x input x batch x C -> O with a k x k kernel, stride 1, pad k/2.
 //
-//   bmm        float operands binarized on the device (pack_matrix) + bmm_pm1 (int32)
+//   bmm        packed operands + bmm_pm1 (int32), B's tensor-core operand re-expanded per call
 //   bmm-bin    packed operands + bmm_pm1_bin with the sign rule (bit output)
 //   bconv      float input binarized (pack_nhwc) + bconv_pm1 (int32 PQNO)
 //   bconv-bin  packed input + bconv_fused with sign thresholds (tau = 0, Geq; bench.hpp:238)
@@ -41,6 +41,19 @@ __global__ void rand_floats_kernel(float* x, size_t n, uint64_t seed) {
 }
 static void rand_words(uint64_t* w, size_t n, uint64_t seed, cudaStream_t st) {
   rand_words_kernel<<<148 * 8, 256, 0, st>>>(w, n, seed);
+  BT_CUDA(cudaGetLastError());
+}
+// Zero the bits past `cols` of each of `rows` rows of `kw` words (matrix pad bits are 0,
+// bit_buffer.hpp:62-66).
+__global__ void clear_pad_kernel(uint64_t* w, size_t rows, size_t kw, size_t cols) {
+  for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (size_t)gridDim.x * blockDim.x)
+    for (size_t i = cols / 64; i < kw; ++i) {
+      const size_t lo = i * 64;
+      w[r * kw + i] &= cols > lo ? (cols - lo >= 64 ? ~0ull : ((1ull << (cols - lo)) - 1ull)) : 0ull;
+    }
+}
+static void clear_pad_bits(uint64_t* w, size_t rows, size_t kw, size_t cols, cudaStream_t st) {
+  clear_pad_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(w, rows, kw, cols);
   BT_CUDA(cudaGetLastError());
 }
 static void rand_floats(float* x, size_t n, uint64_t seed, cudaStream_t st) {
@@ -102,7 +115,7 @@ int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* f
 
 
 int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
-                        size_t engine_len) {
+                        size_t engine_len, const btnn_bench_readback* rb) {
   return guard([&] {
     require(n > 0, BTNN_INVALID_INPUT, "bench_bmm: zero size");
     int dev = 0;
@@ -110,7 +123,7 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
     cudaStream_t st;
     BT_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     const size_t kw = ru(n, 128) / 64;
-    DevBuf a(n * kw * 8), b(n * kw * 8), out_i(bin ? 0 : n * n * 4), out_b(bin ? n * kw * 8 : 0), fa, fb, flag(4);
+    DevBuf a(n * kw * 8), b(n * kw * 8), out_i(bin ? 0 : n * n * 4), out_b(bin ? n * kw * 8 : 0);
     ConvShape s{};
     s.P = s.Q = s.H = s.W = 1;
     s.KH = s.KW = s.stride = 1;
@@ -121,33 +134,45 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
     s.O = (int)n;
     s.f_rps = (int)n;
     s.cwo = (int)kw;
+    // random packed words with the pad bits of every row / column cleared
+    rand_words(a.get<uint64_t>(), n * kw, 1, st);
+    rand_words(b.get<uint64_t>(), n * kw, 2, st);
+    if (n % 128) {
+      clear_pad_bits(a.get<uint64_t>(), n, kw, n, st);
+      clear_pad_bits(b.get<uint64_t>(), n, kw, n, st);
+    }
     Epi e;
     if (bin) {
-      rand_words(a.get<uint64_t>(), n * kw, 1, st);
-      rand_words(b.get<uint64_t>(), n * kw, 2, st);
       e.mode = EPI_BITS;
       e.out_bits = out_b.get<uint64_t>();
     } else {
-      fa.alloc(n * n * 4);
-      fb.alloc(n * n * 4);
-      rand_floats(fa.get<float>(), n * n, 1, st);
-      rand_floats(fb.get<float>(), n * n, 2, st);  // B^T row-major: column j of B contiguous
       e.mode = EPI_I32;
       e.out_i32 = out_i.get<int32_t>();
     }
     TcFilter tcf;
-    if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
+    const bool tc = engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e);
+    if (tc) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
     const char* used = "popc";
+    // the whole bmm_pm1 / bmm_pm1_bin call from packed operands: B is an input of the call,
+    // so its tensor-core operand is re-expanded every time
     auto step = [&] {
-      if (!bin) {
-        launch_pack_rows(fa.get<float>(), n, n, kw * 2, a.get<uint32_t>(), flag.get<int>(), st);
-        launch_pack_rows(fb.get<float>(), n, n, kw * 2, b.get<uint32_t>(), flag.get<int>(), st);
-        if (tcf.valid()) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);  // re-expand the new B
-      }
+      if (tc) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
       used = launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
     };
     BT_CUDA(cudaStreamSynchronize(st));
     time_reps(reps, warmup, st, step, median_ns, min_ns);
+    if (rb && rb->kernel_ns) {  // the GEMM alone (B prepared)
+      double mn = 0;
+      time_reps(reps, warmup, st, [&] { launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf); },
+                rb->kernel_ns, &mn);
+    }
+    if (rb) {
+      BT_CUDA(cudaStreamSynchronize(st));
+      if (rb->a_words) BT_CUDA(cudaMemcpy(rb->a_words, a.get(), a.bytes(), cudaMemcpyDeviceToHost));
+      if (rb->b_words) BT_CUDA(cudaMemcpy(rb->b_words, b.get(), b.bytes(), cudaMemcpyDeviceToHost));
+      if (rb->out) BT_CUDA(cudaMemcpy(rb->out, bin ? out_b.get() : out_i.get(), bin ? out_b.bytes() : out_i.bytes(),
+                                      cudaMemcpyDeviceToHost));
+    }
     if (engine && engine_len) {
       std::snprintf(engine, engine_len, "%s", used);
     }
@@ -156,7 +181,8 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
 }
 
 int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
-                          double* median_ns, double* min_ns, char* engine, size_t engine_len) {
+                          double* median_ns, double* min_ns, char* engine, size_t engine_len,
+                          const btnn_bench_readback* rb) {
   return guard([&] {
     require(input_hw && batch && c && o && k, BTNN_INVALID_INPUT, "bench_bconv: zero size");
     cudaStream_t st;
@@ -222,6 +248,13 @@ int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, siz
     };
     BT_CUDA(cudaStreamSynchronize(st));
     time_reps(reps, warmup, st, step, median_ns, min_ns);
+    if (rb) {
+      BT_CUDA(cudaStreamSynchronize(st));
+      if (rb->a_words) BT_CUDA(cudaMemcpy(rb->a_words, in.get(), in.bytes(), cudaMemcpyDeviceToHost));
+      if (rb->b_words) BT_CUDA(cudaMemcpy(rb->b_words, filt.get(), filt.bytes(), cudaMemcpyDeviceToHost));
+      if (rb->out) BT_CUDA(cudaMemcpy(rb->out, bin ? out_b.get() : out_i.get(), bin ? out_b.bytes() : out_i.bytes(),
+                                      cudaMemcpyDeviceToHost));
+    }
     if (engine && engine_len) std::snprintf(engine, engine_len, "%s", used);
     cudaStreamDestroy(st);
   });

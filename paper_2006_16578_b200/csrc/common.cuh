@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -69,6 +70,18 @@ class DevBuf {
   void* p_ = nullptr;
   size_t n_ = 0;
 };
+
+// Timing experiments (per-role clock64 stamps, work-skipping switches, geometry overrides)
+// exist only in builds made with -DBTNN_TIMING=1 (make TIMING=1). The product build
+// compiles them out, so the kernels carry no debug branches and read no environment knobs.
+#ifndef BTNN_TIMING
+#define BTNN_TIMING 0
+#endif
+inline int timing_knob(const char* name, int dflt) {
+  if (!BTNN_TIMING) return dflt;
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
 
 template <class T>
 DevBuf upload(const T* host, size_t count, cudaStream_t st) {

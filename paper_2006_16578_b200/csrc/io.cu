@@ -23,13 +23,13 @@ namespace {
 using btnn_gpu::fail;
 using btnn_gpu::require;
 
-const char* kind_name(int k) {
+const char* kind_name(int k) {  // model.hpp:25-33
   switch (k) {
-    case BTNN_FIRST_CONV_BWN: return "FirstConvBWN";
-    case BTNN_BIT_CONV: return "BitConv";
-    case BTNN_OR_POOL: return "OrPool";
-    case BTNN_BIT_FC: return "BitFc";
-    case BTNN_LAST_FC: return "LastFc";
+    case BTNN_FIRST_CONV_BWN: return "first_conv";
+    case BTNN_BIT_CONV: return "bit_conv";
+    case BTNN_OR_POOL: return "or_pool";
+    case BTNN_BIT_FC: return "bit_fc";
+    case BTNN_LAST_FC: return "last_fc";
     default: return "?";
   }
 }

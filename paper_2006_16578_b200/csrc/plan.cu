@@ -55,14 +55,21 @@ struct Shard {
   DevBuf x, act[2], fc[2], logits, labels, flag;
   DevBuf rowmax;        // per input row (n, h): largest |x| (tensor-core first conv)
   size_t act_words = 0, fc_words = 0;
-  std::map<std::tuple<size_t, const void*, const void*, const void*>, cudaGraphExec_t> graphs;
+  // Captured graphs per (batch, pointers, engine override). Host-side choices are frozen in
+  // each graph, including which layers stored a pre-averaged tap (restored on replay so
+  // plan_tap_dims / plan_read_tap describe the graph that ran last).
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<char> wrote_half;
+  };
+  std::map<std::tuple<size_t, const void*, const void*, const void*, int>, Graph> graphs;
   std::vector<cudaEvent_t> events;  // breakdown
   cudaStream_t copy_stream = nullptr;    // host->device input chunks (run_shard_host)
   std::vector<cudaEvent_t> in_ready;     // per chunk: input resident
   size_t launches = 0;
   ~Shard() {
     if (device >= 0) cudaSetDevice(device);
-    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto ev : events) cudaEventDestroy(ev);
     for (auto ev : in_ready) cudaEventDestroy(ev);
     if (stream) cudaStreamDestroy(stream);
@@ -279,6 +286,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     fa.P = (int)l.out_h; fa.Q = (int)l.out_w;
     first_tc = engine_override() != BTNN_ENGINE_POPC && first_conv_tc_supported(fa);
   }
+  if (timed) BT_CUDA(cudaEventRecord(sh.events[0], st));  // layer 0's time includes the input pass
   if (first_tc)
     launch_input_rows(d_x, batch * plan->in_h, (int)(plan->in_w * plan->in_c), sh.flag.get<int>(),
                       sh.rowmax.get<uint32_t>(), st);
@@ -293,7 +301,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
   for (size_t i = 0; i < sh.layers.size(); ++i) {
     LayerDev& L = sh.layers[i];
     const btnn_layer_spec& l = L.spec;
-    if (timed) BT_CUDA(cudaEventRecord(sh.events[i], st));
+    if (timed && i > 0) BT_CUDA(cudaEventRecord(sh.events[i], st));
     if (l.kind == BTNN_FIRST_CONV_BWN) {
       uint64_t* out = sh.act[cur].get<uint64_t>();
       // the tensor-core kernel writes every word of its packed output when N % 8 == 0
@@ -439,7 +447,7 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
     sh.launches = enqueue_forward(plan, sh, d_x, batch, d_logits, d_labels, true);
     return;
   }
-  auto key = std::make_tuple(batch, (const void*)d_x, (const void*)d_logits, (const void*)d_labels);
+  auto key = std::make_tuple(batch, (const void*)d_x, (const void*)d_logits, (const void*)d_labels, engine_override());
   auto it = sh.graphs.find(key);
   if (it == sh.graphs.end()) {
     cudaGraph_t g;
@@ -452,13 +460,15 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
       throw;
     }
     BT_CUDA(cudaStreamEndCapture(sh.stream, &g));
-    cudaGraphExec_t ex;
-    BT_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    Shard::Graph gr;
+    BT_CUDA(cudaGraphInstantiate(&gr.exec, g, 0));
     cudaGraphDestroy(g);
     sh.launches = n;
-    it = sh.graphs.emplace(key, ex).first;
+    for (const LayerDev& L : sh.layers) gr.wrote_half.push_back(L.wrote_half);
+    it = sh.graphs.emplace(key, std::move(gr)).first;
   }
-  BT_CUDA(cudaGraphLaunch(it->second, launch_stream ? launch_stream : sh.stream));
+  for (size_t i = 0; i < sh.layers.size(); ++i) sh.layers[i].wrote_half = it->second.wrote_half[i];
+  BT_CUDA(cudaGraphLaunch(it->second.exec, launch_stream ? launch_stream : sh.stream));
 }
 
 // Host-buffer run (the C ABI's run_inference). The input copy is the long pole
@@ -472,8 +482,7 @@ static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t ba
   const size_t xin = plan->in_h * plan->in_w * plan->in_c;
   const bool timed = plan->breakdown && &sh == plan->shards[0].get();
   static const size_t chunk = [] {
-    const char* v = std::getenv("BTNN_E2E_CHUNK");
-    const long c = v ? std::atol(v) : 0;
+    const int c = timing_knob("BTNN_E2E_CHUNK", 0);
     return c > 0 ? (size_t)c : kChunk;
   }();
   const size_t nch = timed ? 1 : std::max<size_t>(1, std::min(kMaxChunks, batch / chunk));

@@ -13,7 +13,7 @@ lib = capi.lib()
 hw, n, c, o = (int(v) for v in (sys.argv[1:5] if len(sys.argv) > 4 else (56, 512, 64, 64)))
 med, mn = C.c_double(), C.c_double()
 eng = C.create_string_buffer(32)
-capi.check(lib.btnn_cuda_bench_bconv(hw, n, c, o, 3, 1, 3, 1, C.byref(med), C.byref(mn), eng, 32))
+capi.check(lib.btnn_cuda_bench_bconv(hw, n, c, o, 3, 1, 3, 1, C.byref(med), C.byref(mn), eng, 32, None))
 ts = np.zeros(4096, dtype=np.uint64)
 capi.check(lib.btnn_cuda_debug_tc_timestamps(ts.ctypes.data_as(C.POINTER(C.c_uint64)), 4096))
 t0 = int(min(v for v in ts if v > 0))
