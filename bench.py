@@ -223,10 +223,10 @@ def ref_run(m, ws, x):
     the checker of the in-run parity field (test infrastructure, never the measured path)."""
     import ctypes as C
 
-    from oracle_lib import ptr
     r, _ = _ref_lib()
     if r is None:
         return None
+    from oracle_lib import ptr
     spec, store = m.c_spec(), ws.c_store()
     n = x.shape[0]
     lg = np.zeros(n * m.classes)

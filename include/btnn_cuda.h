@@ -166,9 +166,10 @@ int btnn_cuda_first_conv_bwn(const float* x, size_t batch, size_t height, size_t
 int btnn_cuda_or_pool(const btnn_act_desc* in, const uint64_t* in_words, size_t window,
                       size_t stride, uint64_t* out_words);
 
-/* Describes the last tensor-core bit GEMM launched from this host thread (kernel-level
+/* Describes the last tensor-core kernel launched from this host thread (kernel-level
  * calls, or plans while their graph is captured): the kernel variant ("halo" or "tmemA",
- * then "/thr", "/bn", "/i32" or "/split", plus "/pg2", "/blocked", "/bres" when they apply),
+ * then "/thr", "/bn", "/i32" or "/split", plus "/pg2", "/blocked", "/bres" when they apply;
+ * "first_conv/stride4" or "first_conv/stride1" for the exact tensor-core first layer),
  * the number of (tile, K-split) work units and the persistent grid size. Tests use it to
  * prove which kernel path and how many tiles per CTA a case exercised. */
 int btnn_cuda_last_tc_launch(char* variant, size_t n, int* units, int* grid);

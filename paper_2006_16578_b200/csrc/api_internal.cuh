@@ -71,5 +71,7 @@ bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter*
 bool tc_supported(const ConvShape& s, const Epi& e);
 void tc_prepare_filter(const ConvShape& s, const uint64_t* filt_plain, TcFilter& out, cudaStream_t st);
 bool launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st);
+// Records a tensor-core first-layer launch for btnn_cuda_last_tc_launch (kernels_first_tc.cu).
+void note_first_conv_launch(int mode, int tiles, int grid);
 
 }  // namespace btnn_gpu

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -22,6 +23,50 @@ thread_local std::string g_last_error;
 thread_local int g_device = 0;
 
 void set_last_error(const std::string& m) { g_last_error = m; }
+
+// Per-thread device scratch for the kernel-level BMM / BConv entry points. cudaMalloc /
+// cudaFree cost 0.1-1 ms per call (and cudaFree synchronizes the device), more than the
+// GEMM itself at the reference's sizes. Every kernel-level call is synchronous (its results
+// are copied back on the legacy stream before it returns), so a call may reuse the previous
+// call's buffers: slots are handed out in call order and only grow.
+struct Scratch {
+  void* p = nullptr;
+  size_t n = 0;
+  template <class T = void>
+  T* get() const {
+    return static_cast<T*>(p);
+  }
+  size_t bytes() const { return n; }
+};
+struct ScratchArena {
+  int device = -1;
+  std::vector<std::unique_ptr<DevBuf>> slots;
+  size_t next = 0;
+  std::unique_ptr<TcFilter> tcf;  // tensor-core operand of the last kernel-level GEMM
+};
+static thread_local ScratchArena g_scratch;
+static void scratch_begin() {
+  int dev = 0;
+  BT_CUDA(cudaGetDevice(&dev));
+  if (dev != g_scratch.device) {
+    g_scratch.slots.clear();
+    g_scratch.tcf.reset();
+    g_scratch.device = dev;
+  }
+  g_scratch.next = 0;
+}
+static Scratch scratch(size_t bytes) {
+  if (g_scratch.next == g_scratch.slots.size()) g_scratch.slots.push_back(std::make_unique<DevBuf>());
+  DevBuf& b = *g_scratch.slots[g_scratch.next++];
+  if (b.bytes() < bytes) b.alloc(bytes + bytes / 4);
+  return Scratch{b.get(), bytes};
+}
+template <class T>
+static Scratch scratch_upload(const T* host, size_t count, cudaStream_t st) {
+  Scratch b = scratch(count * sizeof(T));
+  if (count) BT_CUDA(cudaMemcpyAsync(b.get(), host, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return b;
+}
 
 // FsbGeometry validity as enforced by the BitMatrix / tensor constructors
 // (bit_matrix.hpp:67-74, tensors.hpp:82-85, 130-133).
@@ -144,29 +189,28 @@ static void check_bmm(const btnn_matrix_desc* a, const btnn_matrix_desc* b, cons
 
 // Stage A (RowPacked) and B (ColPacked) on the device, converting fsb operands.
 struct BmmOperands {
-  DevBuf a, b;
+  Scratch a, b;
   ConvShape s{};
 };
 static BmmOperands stage_bmm(const btnn_matrix_desc* a, const uint64_t* aw, const btnn_matrix_desc* b,
                              const uint64_t* bw, cudaStream_t st) {
   BmmOperands op;
-  DevBuf ta = upload(aw, mat_words(a->rows, a->cols, a->layout, a->bh, a->bw), st);
-  DevBuf tb = upload(bw, mat_words(b->rows, b->cols, b->layout, b->bh, b->bw), st);
+  Scratch ta = scratch_upload(aw, mat_words(a->rows, a->cols, a->layout, a->bh, a->bw), st);
+  Scratch tb = scratch_upload(bw, mat_words(b->rows, b->cols, b->layout, b->bh, b->bw), st);
   if (a->layout == BTNN_ROW_PACKED) {
-    op.a = std::move(ta);
+    op.a = ta;
   } else {
-    op.a.alloc(mat_words(a->rows, a->cols, BTNN_ROW_PACKED, 0, 0) * 8);
+    op.a = scratch(mat_words(a->rows, a->cols, BTNN_ROW_PACKED, 0, 0) * 8);
     launch_convert_matrix(a->rows, a->cols, a->layout, a->bh, a->bw, ta.get<uint64_t>(), BTNN_ROW_PACKED, 0, 0,
                           op.a.get<uint64_t>(), st);
   }
   if (b->layout == BTNN_COL_PACKED) {
-    op.b = std::move(tb);
+    op.b = tb;
   } else {
-    op.b.alloc(mat_words(b->rows, b->cols, BTNN_COL_PACKED, 0, 0) * 8);
+    op.b = scratch(mat_words(b->rows, b->cols, BTNN_COL_PACKED, 0, 0) * 8);
     launch_convert_matrix(b->rows, b->cols, b->layout, b->bh, b->bw, tb.get<uint64_t>(), BTNN_COL_PACKED, 0, 0,
                           op.b.get<uint64_t>(), st);
   }
-  BT_CUDA(cudaStreamSynchronize(st));  // temporaries die at scope exit
   ConvShape& s = op.s;
   s.P = s.Q = s.H = s.W = 1;
   s.KH = s.KW = s.stride = 1;
@@ -181,7 +225,10 @@ static BmmOperands stage_bmm(const btnn_matrix_desc* a, const uint64_t* aw, cons
   return op;
 }
 
-static void use_device() { BT_CUDA(cudaSetDevice(g_device)); }
+static void use_device() {
+  BT_CUDA(cudaSetDevice(g_device));
+  scratch_begin();
+}
 
 // One implicit GEMM for a kernel-level call: the tensor-core operand is expanded from
 // the caller's filter for this call (a plan does it once at creation).
@@ -189,11 +236,11 @@ static const char* run_gemm(const ConvShape& s0, const uint64_t* act, const uint
                             cudaStream_t st) {
   ConvShape s = s0;
   s.halo_ok = s.C <= 128;
-  TcFilter tcf;
-  if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, filt, tcf, st);
-  const char* engine = launch_bgemm(s, act, filt, e, st, EngineHint::Auto, &tcf);
-  BT_CUDA(cudaStreamSynchronize(st));  // tcf is released at scope exit
-  return engine;
+  if (!g_scratch.tcf) g_scratch.tcf = std::make_unique<TcFilter>();
+  TcFilter& tcf = *g_scratch.tcf;
+  const bool tc = engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e);
+  if (tc) tc_prepare_filter(s, filt, tcf, st);
+  return launch_bgemm(s, act, filt, e, st, EngineHint::Auto, tc ? &tcf : nullptr);
 }
 
 }  // namespace btnn_gpu
@@ -401,7 +448,7 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
     BmmOperands op = stage_bmm(a, aw, b, bw, st);
     Epi e;
     if (which < 2) {
-      DevBuf o(a->rows * b->cols * 4);
+      Scratch o = scratch(a->rows * b->cols * 4);
       e.mode = EPI_I32;
       e.raw = which == 0;
       e.out_i32 = o.get<int32_t>();
@@ -409,15 +456,15 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
       BT_CUDA(cudaMemcpy(out, o.get(), a->rows * b->cols * 4, cudaMemcpyDeviceToHost));
       return;
     }
-    DevBuf dlo, dhi;
+    Scratch dlo, dhi;
     if (n_thr) {
-      dlo = upload(lo.data(), n_thr, st);
-      dhi = upload(hi.data(), n_thr, st);
+      dlo = scratch_upload(lo.data(), n_thr, st);
+      dhi = scratch_upload(hi.data(), n_thr, st);
       e.thr_lo = dlo.get<long long>();
       e.thr_hi = dhi.get<long long>();
     }
     const size_t rp_words = a->rows * (size_t)op.s.cwo;
-    DevBuf rp(rp_words * 8);
+    Scratch rp = scratch(rp_words * 8);
     BT_CUDA(cudaMemsetAsync(rp.get(), 0, rp.bytes(), st));
     e.mode = EPI_BITS;
     e.out_bits = rp.get<uint64_t>();
@@ -428,7 +475,7 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
       BT_CUDA(cudaMemcpy(out, rp.get(), words * 8, cudaMemcpyDeviceToHost));
       return;
     }
-    DevBuf o(words * 8);
+    Scratch o = scratch(words * 8);
     launch_convert_matrix(a->rows, b->cols, BTNN_ROW_PACKED, 0, 0, rp.get<uint64_t>(), out_layout, a->bh, a->bw,
                           o.get<uint64_t>(), st);
     BT_CUDA(cudaMemcpy(out, o.get(), words * 8, cudaMemcpyDeviceToHost));
@@ -463,23 +510,23 @@ static void check_conv(const btnn_act_desc* in, const btnn_filter_desc* f, const
 }
 
 struct ConvOperands {
-  DevBuf in, filt;
+  Scratch in, filt;
   ConvShape s{};
 };
 static ConvOperands stage_conv(const btnn_act_desc* in, const uint64_t* iw, const btnn_filter_desc* f,
                                const uint64_t* fw, const btnn_conv_geom* g, size_t P, size_t Q, cudaStream_t st) {
   ConvOperands op;
-  DevBuf ti = upload(iw, btnn_cuda_act_words(in), st);
-  DevBuf tf = upload(fw, btnn_cuda_filter_words(f), st);
+  Scratch ti = scratch_upload(iw, btnn_cuda_act_words(in), st);
+  Scratch tf = scratch_upload(fw, btnn_cuda_filter_words(f), st);
   if (!in->tiled) {
-    op.in = std::move(ti);
-    op.filt = std::move(tf);
+    op.in = ti;
+    op.filt = tf;
   } else {
-    op.in.alloc(act_words(in->height, in->width, in->batch, in->channels, 0, 0, 0) * 8);
+    op.in = scratch(act_words(in->height, in->width, in->batch, in->channels, 0, 0, 0) * 8);
     launch_convert_act(in->height, in->width, in->batch, in->channels, 1, in->bh, in->bw, ti.get<uint64_t>(), 0, 0, 0,
                        op.in.get<uint64_t>(), st);
     // Filter planes share the activation plane geometry with n -> o (tensors.hpp:143-147).
-    op.filt.alloc(filt_words(f->kh, f->kw, f->out_channels, f->in_channels, 0, 0, 0) * 8);
+    op.filt = scratch(filt_words(f->kh, f->kw, f->out_channels, f->in_channels, 0, 0, 0) * 8);
     launch_convert_act(f->kh, f->kw, f->out_channels, f->in_channels, 1, f->bh, f->bw, tf.get<uint64_t>(), 0, 0, 0,
                        op.filt.get<uint64_t>(), st);
     BT_CUDA(cudaStreamSynchronize(st));
@@ -511,7 +558,7 @@ int btnn_cuda_bconv_pm1(const btnn_act_desc* in, const uint64_t* iw, const btnn_
     cudaStream_t st = 0;
     ConvOperands op = stage_conv(in, iw, f, fw, g, P, Q, st);
     const size_t n_out = P * Q * in->batch * f->out_channels;
-    DevBuf o(n_out * 4);
+    Scratch o = scratch(n_out * 4);
     Epi e;
     e.mode = EPI_I32;
     e.out_i32 = o.get<int32_t>();
@@ -544,16 +591,16 @@ int btnn_cuda_bconv_fused(const btnn_act_desc* in, const uint64_t* iw, const btn
     cudaStream_t st = 0;
     ConvOperands op = stage_conv(in, iw, f, fw, g, P, Q, st);
     const size_t n_out = P * Q * in->batch * O;
-    DevBuf dlo, dhi, dbn, drin, drout;
+    Scratch dlo, dhi, dbn, drin, drout;
     Epi e;
     e.mode = EPI_BITS;
     if (thresholded) {
-      dlo = upload(lo.data(), O, st);
-      dhi = upload(hi.data(), O, st);
+      dlo = scratch_upload(lo.data(), O, st);
+      dhi = scratch_upload(hi.data(), O, st);
       e.thr_lo = dlo.get<long long>();
       e.thr_hi = dhi.get<long long>();
     } else {
-      dbn = upload(bnp.data(), bnp.size(), st);
+      dbn = scratch_upload(bnp.data(), bnp.size(), st);
       launch_bn_recip(dbn.get<double>(), (int)O, st);
       e.bn_mean = dbn.get<double>();
       e.bn_s = e.bn_mean + O;
@@ -562,16 +609,16 @@ int btnn_cuda_bconv_fused(const btnn_act_desc* in, const uint64_t* iw, const btn
       e.bn_rcp = e.bn_mean + 4 * O;
     }
     if (fu->residual_in) {
-      drin = upload(fu->residual_in, n_out, st);
+      drin = scratch_upload(fu->residual_in, n_out, st);
       e.rin = drin.get<double>();
       e.rin_P = (int)P; e.rin_Q = (int)Q; e.rin_C = (int)O; e.rin_halve = 0;
     }
     if (fu->residual_out) {
-      drout.alloc(n_out * 8);
+      drout = scratch(n_out * 8);
       e.rout = drout.get<double>();
     }
     const size_t plain_words = act_words(P, Q, in->batch, O, 0, 0, 0);
-    DevBuf ob(plain_words * 8);
+    Scratch ob = scratch(plain_words * 8);
     BT_CUDA(cudaMemsetAsync(ob.get(), 0, ob.bytes(), st));
     e.out_bits = ob.get<uint64_t>();
     run_gemm(op.s, op.in.get<uint64_t>(), op.filt.get<uint64_t>(), e, st);
@@ -580,7 +627,7 @@ int btnn_cuda_bconv_fused(const btnn_act_desc* in, const uint64_t* iw, const btn
       BT_CUDA(cudaMemcpyAsync(out, ob.get(), plain_words * 8, cudaMemcpyDeviceToHost, st));
     } else {
       const size_t words = act_words(P, Q, in->batch, O, 1, in->bh, in->bw);
-      DevBuf t(words * 8);
+      Scratch t = scratch(words * 8);
       launch_convert_act(P, Q, in->batch, O, 0, 0, 0, ob.get<uint64_t>(), 1, in->bh, in->bw, t.get<uint64_t>(), st);
       BT_CUDA(cudaMemcpyAsync(out, t.get(), words * 8, cudaMemcpyDeviceToHost, st));
       BT_CUDA(cudaStreamSynchronize(st));

@@ -82,8 +82,9 @@ bool encode_f64_map(CUtensorMap* m, const double* base, const uint64_t dims[4], 
                     const uint32_t box[4], bool swizzle128 = true);
 
 bool first_conv_tc_supported(const FirstConvArgs& a);
-size_t first_conv_tc_weight_bytes(int KH, int KW);
-void launch_first_conv_tc_weights(const float* w_pm1, int O, int KH, int KW, int C, int8_t* out, cudaStream_t st);
+size_t first_conv_tc_weight_bytes(int KH, int KW, int O, int stride);
+void launch_first_conv_tc_weights(const float* w_pm1, int O, int KH, int KW, int C, int stride, int8_t* out,
+                                  cudaStream_t st);
 // Input check per row (n, h) of W*C floats: non-finite flag + largest |x| bit pattern.
 void launch_input_rows(const float* x, size_t rows, int row_len, int* flag, uint32_t* rowmax, cudaStream_t st);
 // rowmax from launch_input_rows; fix_list holds up to N*P*Q window ids.

@@ -189,9 +189,9 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
       const int K = (int)(l.kh * l.kw * l.in_channels);
       L.wbits.alloc(first_conv_signbits_words((int)l.out_channels, K) * 4);
       launch_first_conv_signbits(L.wpm1.get<float>(), (int)l.out_channels, K, L.wbits.get<uint32_t>(), st);
-      L.wblk.alloc(first_conv_tc_weight_bytes((int)l.kh, (int)l.kw));
+      L.wblk.alloc(first_conv_tc_weight_bytes((int)l.kh, (int)l.kw, (int)l.out_channels, (int)l.stride));
       launch_first_conv_tc_weights(L.wpm1.get<float>(), (int)l.out_channels, (int)l.kh, (int)l.kw,
-                                   (int)l.in_channels, L.wblk.get<int8_t>(), st);
+                                   (int)l.in_channels, (int)l.stride, L.wblk.get<int8_t>(), st);
       L.fix_list.alloc(B * l.out_h * l.out_w * sizeof(int));
       L.fix_count.alloc(sizeof(int));
       sh.rowmax.alloc(B * l.in_h * sizeof(uint32_t));
@@ -284,6 +284,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     fa.N = (int)batch; fa.H = (int)l.in_h; fa.W = (int)l.in_w; fa.C = (int)l.in_channels; fa.O = (int)l.out_channels;
     fa.KH = (int)l.kh; fa.KW = (int)l.kw; fa.stride = (int)l.stride; fa.pad = (int)l.pad;
     fa.P = (int)l.out_h; fa.Q = (int)l.out_w;
+    fa.tap = l.residual_out ? sh.layers[0].tap.get<double>() : nullptr;  // (sizes the tap stage)
     first_tc = engine_override() != BTNN_ENGINE_POPC && first_conv_tc_supported(fa);
   }
   if (timed) BT_CUDA(cudaEventRecord(sh.events[0], st));  // layer 0's time includes the input pass

@@ -244,8 +244,11 @@ def _oracle_first_conv(x, wpm, k, o, s, pd):
     return want
 
 
-@pytest.mark.parametrize("n,hw,k,o,pd", [(3, 224, 7, 64, 3), (2, 61, 11, 48, 5), (4, 36, 5, 16, 2)])
-def test_first_conv_exact_digits_adversarial(n, hw, k, o, pd):
+@pytest.mark.parametrize("n,hw,k,o,pd,st", [(3, 224, 7, 64, 3, 4), (2, 61, 11, 48, 5, 4), (4, 36, 5, 16, 2, 4),
+                                             (2, 224, 11, 128, 5, 4), (3, 40, 7, 100, 3, 4), (4, 32, 3, 128, 1, 1),
+                                             (3, 30, 3, 72, 1, 1), (5, 17, 3, 20, 1, 1), (2, 33, 4, 40, 1, 1),
+                                             (3, 28, 3, 128, 0, 1)])
+def test_first_conv_exact_digits_adversarial(n, hw, k, o, pd, st, engine):
     """The tensor-core first layer (integer digit MMAs, kernels_first_tc.cu) is exact only
     on a per-tile grid; inputs here put values off that grid (tiny and subnormal values
     next to large ones, signed zeros, powers of two, an all-zero image, a huge outlier) so
@@ -266,6 +269,8 @@ def test_first_conv_exact_digits_adversarial(n, hw, k, o, pd):
         flat[2, idx[26]] = np.float32(3e20)
         flat[2, idx[27:40]] = rng.standard_normal(13).astype(np.float32) * np.float32(1e-6)
     wpm = np.where(rng.standard_normal(o * k * k * 3) >= 0, 1.0, -1.0).astype(np.float32)
-    got = B.first_conv_bwn(x, wpm, k, k, o, capi.ConvGeom(k, k, 4, pd))
-    want = _oracle_first_conv(x, wpm, k, o, 4, pd)
+    got = B.first_conv_bwn(x, wpm, k, k, o, capi.ConvGeom(k, k, st, pd))
+    if engine == "tc":  # the exact tensor-core kernel covers these shapes
+        assert capi.last_tc_launch()[0] == f"first_conv/stride{st}", capi.last_tc_launch()
+    want = _oracle_first_conv(x, wpm, k, o, st, pd)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
