@@ -205,10 +205,13 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
                            L.filt.get<uint64_t>(), st);
         BT_CUDA(cudaStreamSynchronize(st));
       }
-      // Halo-mode kernels for every conv (C <= 128); a tap producer whose consumer halves the
-      // tap runs them in pair mode (kernels_tc.cu), or the TMEM-A path in 2x2-blocked row
-      // order when the pair geometry does not apply — both read this filter layout.
+      // Halo-mode kernels for every conv except a tap producer whose consumer halves it
+      // (that one writes the pre-averaged tap in 2x2-blocked row order, TMEM-A path).
       L.halo_ok = true;
+      if (l.residual_out)
+        for (size_t j = i + 1; j < m->n_layers; ++j)
+          if (m->layers[j].residual_in && m->layers[j].shortcut_from == (int)i && m->layers[j].out_h != l.out_h)
+            L.halo_ok = false;
       tc_prepare_filter(conv_shape(l, B, L.halo_ok), L.filt.get<uint64_t>(), L.tc, st);
     } else if (l.kind == BTNN_BIT_FC || l.kind == BTNN_LAST_FC) {
       DevBuf raw = upload(w.fc_words, w.fc_n_words, st);
