@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbtnn_cuda.so")
+# BTNN_LIB selects another build of the library (the timing-experiment build, Makefile)
+LIB_PATH = os.environ.get("BTNN_LIB") or os.path.join(_HERE, "libbtnn_cuda.so")
 
 BTNN_OK, BTNN_INVALID_INPUT, BTNN_UNSUPPORTED_SHAPE, BTNN_IO_ERROR, BTNN_VALIDATION_ERROR, BTNN_CUDA_ERROR = range(6)
 ROW_PACKED, COL_PACKED, FSB_ROW, FSB_COL = range(4)

@@ -25,7 +25,7 @@
 
 namespace btnn_gpu {
 
-constexpr size_t kChunk = 64, kMaxChunks = 8;  // run_shard_host input pipelining (BTNN_E2E_CHUNK overrides)
+constexpr size_t kMaxChunks = 16;  // run_shard_host input pipelining (chunk_schedule)
 
 struct LayerDev {
   btnn_layer_spec spec{};
@@ -472,33 +472,55 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
   BT_CUDA(cudaGraphLaunch(it->second.exec, launch_stream ? launch_stream : sh.stream));
 }
 
-// Host-buffer run (the C ABI's run_inference). The input copy is the long pole
-// end to end (602 KB per ImageNet image over PCIe), so the batch is cut into chunks of
-// ~kChunk images: chunk k+1's host->device copy runs on the copy stream while chunk k's
-// graph runs on the compute stream. Samples are independent, so chunking does not change
-// any result.
+// Host-buffer run (the C ABI's run_inference). The input copy is the long pole end to end
+// (602 KB per ImageNet image over PCIe, ~55 GB/s measured: ~90 K img/s), so the batch is cut
+// into chunks: chunk k+1's host->device copy runs on the copy stream while chunk k's graph
+// runs on the compute stream. Samples are independent, so chunking does not change any result.
+//
+// The step ends when the last chunk's copy and then its compute finish. Big chunks run the
+// network efficiently (a 128-image graph computes ~1.4x faster than its copy arrives; a
+// 64-image one barely keeps pace) while a small last chunk keeps the exposed compute tail
+// short, so the schedule takes chunks of up to 128 images while more than two remain, then
+// halves them down to 16: batch 512 -> 128 128 128 64 32 16 16.
+static std::vector<size_t> chunk_schedule(size_t batch) {
+  std::vector<size_t> sizes;
+  static const size_t fixed = (size_t)timing_knob("BTNN_E2E_CHUNK", 0);  // timing experiments
+  if (fixed) {
+    for (size_t b0 = 0; b0 < batch; b0 += fixed) sizes.push_back(std::min(fixed, batch - b0));
+    return sizes;
+  }
+  // (large batches: bigger base chunks so the whole schedule fits kMaxChunks events)
+  const size_t base = std::max<size_t>({16, std::min<size_t>(128, ru(batch / 4, 8)), ru(batch / 12, 8)});
+  size_t r = batch;
+  while (r > 2 * base && sizes.size() + 6 < kMaxChunks) {
+    sizes.push_back(base);
+    r -= base;
+  }
+  while (r > 16 && sizes.size() + 2 < kMaxChunks) {
+    const size_t c = std::min(r, ru(cdiv(r, 2), 8));
+    sizes.push_back(c);
+    r -= c;
+  }
+  if (r) sizes.push_back(r);
+  return sizes;
+}
 
 static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t batch, double* logits, int32_t* labels) {
   BT_CUDA(cudaSetDevice(sh.device));
   const size_t xin = plan->in_h * plan->in_w * plan->in_c;
   const bool timed = plan->breakdown && &sh == plan->shards[0].get();
-  static const size_t chunk = [] {
-    const int c = timing_knob("BTNN_E2E_CHUNK", 0);
-    return c > 0 ? (size_t)c : kChunk;
-  }();
-  const size_t nch = timed ? 1 : std::max<size_t>(1, std::min(kMaxChunks, batch / chunk));
-  const size_t per = cdiv(batch, nch);
+  const std::vector<size_t> sizes = timed ? std::vector<size_t>{batch} : chunk_schedule(batch);
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
-  for (size_t k = 0; k < nch; ++k) {
-    const size_t b0 = k * per;
-    if (b0 >= batch) break;
-    const size_t bn = std::min(per, batch - b0);
+  size_t b0 = 0;
+  for (size_t k = 0; k < sizes.size(); ++k) {
+    const size_t bn = sizes[k];
     float* dx = sh.x.get<float>() + b0 * xin;
     BT_CUDA(cudaMemcpyAsync(dx, x + b0 * xin, bn * xin * sizeof(float), cudaMemcpyHostToDevice, sh.copy_stream));
     BT_CUDA(cudaEventRecord(sh.in_ready[k], sh.copy_stream));
     BT_CUDA(cudaStreamWaitEvent(sh.stream, sh.in_ready[k], 0));
     run_shard_device(plan, sh, dx, bn, sh.logits.get<double>() + b0 * plan->classes, sh.labels.get<int32_t>() + b0,
                      timed);
+    b0 += bn;
   }
   int bad = 0;
   BT_CUDA(cudaMemcpyAsync(&bad, sh.flag.get(), sizeof(int), cudaMemcpyDeviceToHost, sh.stream));

@@ -83,6 +83,14 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, const void* src, 
                : "memory");
 }
 
+// Prefetch a tensor box into L2 (no shared memory, no completion tracking): a later
+// tma_load_4d of the same box then hits L2 instead of HBM.
+__device__ __forceinline__ void tma_prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(tmap), "r"(c0), "r"(c1),
+               "r"(c2), "r"(c3)
+               : "memory");
+}
+
 // ---- TMEM -------------------------------------------------------------------------
 // One warp allocates (power of two >= 32 columns); the base address lands in smem.
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
