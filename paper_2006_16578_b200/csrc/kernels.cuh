@@ -49,6 +49,9 @@ struct Epi {
                                      //   tensor-core engine split few-tile FC GEMMs along K
   double* rout_half = nullptr;       // residual_out pre-averaged for a halving consumer,
                                      //   PQNO over (P/2, Q/2, N, O) (tensor-core engine only)
+  int pool = 0;                      // fused or_pool (bconv.hpp:247-272) with window = stride = pool:
+                                     //   bits are OR-ed (atomicOr) into the pooled site (p/pool, q/pool)
+                                     //   of a zeroed (P/pool, Q/pool) tensor (tensor-core engine only)
 };
 
 // CUDA-core LOP3+POPC implicit GEMM (any shape). act/filt are device pointers.
@@ -68,6 +71,7 @@ struct FirstConvArgs {
   uint64_t* out_bits;     // optional, HWNC plain (pre-zeroed)
   int out_rps, cwo;
   const uint32_t* wbits = nullptr;  // optional per-o sign bits (launch_first_conv_signbits)
+  int pool = 0;                     // fused or_pool with window = stride = pool (see Epi::pool)
 };
 void launch_first_conv(const FirstConvArgs& a, cudaStream_t st);
 size_t first_conv_signbits_words(int O, int K);

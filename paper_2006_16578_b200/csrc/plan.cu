@@ -44,6 +44,7 @@ struct LayerDev {
   bool feeds_full = false, feeds_half = false;  // consumers read the tap as is / halved
   bool wrote_half = false;                      // last enqueue stored tap_half instead of tap
   bool halo_ok = false;                         // conv may run the halo-mode kernel (filter layout)
+  bool pool_fused = false;                      // or_pool layer folded into the previous conv's epilogue
   std::string engine = "-";
 };
 
@@ -268,6 +269,19 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
   BT_CUDA(cudaStreamSynchronize(st));
 }
 
+// Window of an or_pool layer i + 1 that the conv layer i can fold into its epilogue
+// (non-overlapping windows that tile the conv's grid exactly: each output site feeds one
+// pooled site), else 0.
+static int fusable_pool(const Shard& sh, size_t i) {
+  if (i + 1 >= sh.layers.size()) return 0;
+  const btnn_layer_spec& l = sh.layers[i].spec;
+  const btnn_layer_spec& nx = sh.layers[i + 1].spec;
+  if (nx.kind != BTNN_OR_POOL || nx.window != nx.pool_stride || nx.window < 2) return 0;
+  if (l.out_h % nx.window || l.out_w % nx.window || nx.out_h * nx.window != l.out_h || nx.out_w * nx.window != l.out_w)
+    return 0;
+  return (int)nx.window;
+}
+
 // Enqueues the whole layer sequence for `batch` samples of x (device) on the shard's
 // stream. Returns the number of kernels launched.
 static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size_t batch, double* d_logits,
@@ -305,8 +319,13 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     if (timed && i > 0) BT_CUDA(cudaEventRecord(sh.events[i], st));
     if (l.kind == BTNN_FIRST_CONV_BWN) {
       uint64_t* out = sh.act[cur].get<uint64_t>();
-      // the tensor-core kernel writes every word of its packed output when N % 8 == 0
-      if (!(first_tc && np == batch))
+      const int pool = first_tc ? fusable_pool(sh, i) : 0;
+      if (i + 1 < sh.layers.size()) sh.layers[i + 1].pool_fused = pool != 0;
+      // the tensor-core kernel writes every word of its packed output when N % 8 == 0; a fused
+      // pool ORs into a zeroed pooled tensor
+      if (pool)
+        BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h / pool, l.out_w / pool, batch, l.out_channels, 0, 0, 0) * 8, st));
+      else if (!(first_tc && np == batch))
         BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
       FirstConvArgs a{};
       a.x = d_x;
@@ -322,11 +341,12 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       a.wbits = L.wbits.get<uint32_t>();
       a.out_rps = (int)np;
       a.cwo = (int)(act_cpad(l.out_channels, 0, 0) / 64);
+      a.pool = pool;
       if (first_tc) {
         launch_first_conv_tc(a, sh.rowmax.get<uint32_t>(), L.wblk.get<int8_t>(), L.fix_count.get<int>(),
                              L.fix_list.get<int>(), st);
         launches += 2;
-        L.engine = "tc_i8_exact";
+        L.engine = pool ? "tc_i8_exact+pool" : "tc_i8_exact";
       } else {
         launch_first_conv(a, st);
         ++launches;
@@ -377,13 +397,23 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         }
       }
       // The packed output is cleared first unless the tensor-core epilogue writes every word of
-      // it (channel-pad words included): no image padding (N a multiple of 8).
-      if (!(will_use_tc(s, e, EngineHint::Auto, &L.tc) && np == batch))
+      // it (channel-pad words included): no image padding (N a multiple of 8). A following
+      // or_pool is folded into the tensor-core epilogue (atomic OR into the zeroed pooled tensor).
+      const bool tc = will_use_tc(s, e, EngineHint::Auto, &L.tc);
+      e.pool = tc ? fusable_pool(sh, i) : 0;
+      if (i + 1 < sh.layers.size()) sh.layers[i + 1].pool_fused = e.pool != 0;
+      if (e.pool)
+        BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h / e.pool, l.out_w / e.pool, batch, l.out_channels, 0, 0, 0) * 8, st));
+      else if (!(tc && np == batch))
         BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
       L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
+      if (e.pool) L.engine += "+pool";
       ++launches;
       cur ^= 1;
       H = l.out_h; W = l.out_w; C = l.out_channels;
+    } else if (l.kind == BTNN_OR_POOL && L.pool_fused) {
+      L.engine = "fused";  // done by the previous conv's epilogue
+      H = l.out_h; W = l.out_w;
     } else if (l.kind == BTNN_OR_POOL) {
       const size_t pw = np * act_cpad(C, 0, 0) / 64;
       launch_or_pool(sh.act[cur].get<uint64_t>(), (int)H, (int)W, pw, (int)l.window, (int)l.pool_stride, (int)l.out_h,
@@ -482,13 +512,16 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
 // 64-image one barely keeps pace) while a small last chunk keeps the exposed compute tail
 // short, so the schedule takes chunks of up to 128 images while more than two remain, then
 // halves them down to 16: batch 512 -> 128 128 128 64 32 16 16.
-static std::vector<size_t> chunk_schedule(size_t batch) {
+static std::vector<size_t> chunk_schedule(size_t batch, size_t in_bytes_per_image) {
   std::vector<size_t> sizes;
   static const size_t fixed = (size_t)timing_knob("BTNN_E2E_CHUNK", 0);  // timing experiments
   if (fixed) {
     for (size_t b0 = 0; b0 < batch; b0 += fixed) sizes.push_back(std::min(fixed, batch - b0));
     return sizes;
   }
+  // Small batches are latency-bound, and small inputs (Cifar 12 KB, MNIST 3 KB per image)
+  // copy in a fraction of the compute time: one graph each.
+  if (batch < 128 || in_bytes_per_image < 64 * 1024) return {batch};
   // (large batches: bigger base chunks so the whole schedule fits kMaxChunks events)
   const size_t base = std::max<size_t>({16, std::min<size_t>(128, ru(batch / 4, 8)), ru(batch / 12, 8)});
   size_t r = batch;
@@ -509,7 +542,7 @@ static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t ba
   BT_CUDA(cudaSetDevice(sh.device));
   const size_t xin = plan->in_h * plan->in_w * plan->in_c;
   const bool timed = plan->breakdown && &sh == plan->shards[0].get();
-  const std::vector<size_t> sizes = timed ? std::vector<size_t>{batch} : chunk_schedule(batch);
+  const std::vector<size_t> sizes = timed ? std::vector<size_t>{batch} : chunk_schedule(batch, xin * sizeof(float));
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
   size_t b0 = 0;
   for (size_t k = 0; k < sizes.size(); ++k) {
