@@ -308,6 +308,20 @@ int btnn_cuda_plan_tap_dims(btnn_plan* plan, size_t i, size_t* dims);
 const char* btnn_cuda_plan_layer_engine(btnn_plan* plan, size_t i);
 int btnn_cuda_plan_destroy(btnn_plan* plan);
 
+/* ---- BENN ensembles ---------------------------- */
+/* Combine K member outputs on the device. d_logits: K x batch x classes f64 (member-major,
+ * as K plan_run_device calls leave them), d_labels: K x batch. Members fold in member order:
+ *   HARD        votes[c] = #{k : label_k == c} (as f64)
+ *   SOFT        mean[c] = (((l_0 + l_1) + ...) + l_{K-1}) / K
+ *   BOOST       score[c] = sum_k (label_k == c ? alpha_k : 0)  (weighted vote)
+ *   BOOST_SOFT  score[c] = sum_k fl(alpha_k * l_k[c])
+ * then the first-max label per row (inference.hpp:177-184). alpha: host array of K member
+ * weights (boosting modes). Outputs are device pointers; async on `stream` (NULL = legacy). */
+enum { BTNN_BENN_HARD = 0, BTNN_BENN_SOFT = 1, BTNN_BENN_BOOST = 2, BTNN_BENN_BOOST_SOFT = 3 };
+int btnn_cuda_benn_combine(const double* d_logits, const int32_t* d_labels, size_t members, size_t batch,
+                           size_t classes, const double* alpha, int mode, double* d_scores, int32_t* d_out_labels,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -236,6 +236,8 @@ class Plan:
         self.classes = self._spec.classes
         self.n_layers = self._spec.n_layers
         self.in_dims = (self._spec.in_h, self._spec.in_w, self._spec.in_c)
+        self.devices = tuple(devices)
+        self.device = devices[0] if len(devices) == 1 else -1  # -1: sharded over devices
 
     def run(self, x: np.ndarray):
         x = np.ascontiguousarray(x, dtype=np.float32)

@@ -37,18 +37,29 @@ def main():
         for i, h in enumerate(hdr):
             if i < 4:
                 continue
-            if h == "Warp Stall Sampling (All Samples)" or (h.startswith("stall_") and "Not Issued" not in h):
+            if h in ("Warp Stall Sampling (All Samples)", "Instructions Executed") or (h.startswith("stall_") and "Not Issued" not in h):
                 try:
                     agg[key][h] += float(r[i])
                 except ValueError:
                     pass
     tot = sum(v["Warp Stall Sampling (All Samples)"] for v in agg.values())
+    itot = sum(v["Instructions Executed"] for v in agg.values())
+    print(f"total warp instructions executed {itot:.0f}")
+    if len(sys.argv) > 3:  # per line-range totals: file:lo-hi,... (instructions, stall samples)
+        for spec in sys.argv[3].split(","):
+            f, rng = spec.split(":")
+            lo, hi = map(int, rng.split("-"))
+            ins = sum(v["Instructions Executed"] for (ff, ln), v in agg.items() if ff == f and lo <= ln <= hi)
+            smp = sum(v["Warp Stall Sampling (All Samples)"] for (ff, ln), v in agg.items() if ff == f and lo <= ln <= hi)
+            print(f"  {spec:30s} instr {100 * ins / max(itot, 1):5.1f}%  samples {100 * smp / max(tot, 1):5.1f}%")
     hot = sorted(agg.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:top]
+    print("-- hottest by stall samples (i = share of executed instructions)")
     for (f, ln), v in hot:
         s = v["Warp Stall Sampling (All Samples)"]
         reasons = sorted(((k[6:], x) for k, x in v.items() if k.startswith("stall_")), key=lambda t: -t[1])[:3]
         rs = " ".join(f"{k}:{100 * x / max(s, 1):.0f}%" for k, x in reasons if x > 0)
-        print(f"{100 * s / tot:5.1f}% {f}:{ln:<5} {rs:40s} {text.get((f, ln), '')[:70]}")
+        ins = v["Instructions Executed"]
+        print(f"{100 * s / tot:5.1f}% i{100 * ins / max(itot, 1):5.1f}% {f}:{ln:<5} {rs:40s} {text.get((f, ln), '')[:70]}")
 
 
 if __name__ == "__main__":
