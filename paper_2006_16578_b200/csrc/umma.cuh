@@ -34,6 +34,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Wait for a role that is not on the critical path (producers / MMA issuer of an
+// epilogue-bound kernel): a failed poll sleeps ~ns nanoseconds (plain NANOSLEEP, not woken by
+// other barriers' traffic), so the waiting warp does not take issue slots from the epilogue.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+template <int NS = 256>
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(NS);
+}
+
 // One elected lane of a converged warp (elect.sync).
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
