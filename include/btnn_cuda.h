@@ -195,13 +195,15 @@ int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* f
  * b = plain KKOC filter words, out = int32 PQNO (bconv) or HWNC bits (bconv-bin).
  * kernel_ns (bmm only) receives the GEMM alone with B already expanded, and stream_ns the
  * whole call, each averaged over `reps` launches back to back between two events (the host
- * launch cost overlapped, as in a stream of calls). */
+ * launch cost overlapped, as in a stream of calls); graph_ns the whole call with `reps` calls
+ * captured in one CUDA graph and replayed (device time per call, no host launch in it). */
 typedef struct {
   uint64_t* a_words;
   uint64_t* b_words;
   void* out;
   double* kernel_ns;
   double* stream_ns;
+  double* graph_ns;
 } btnn_bench_readback;
 /* bench_bmm: n x n x n on random packed +-1 words (bench.hpp:76-87, 136-137); bin = 0 ->
  * "bmm" (bmm_pm1, int32 out), bin = 1 -> "bmm-bin" (bmm_pm1_bin sign rule, bit output).

@@ -56,7 +56,8 @@ class ConvFused(C.Structure):
 
 class BenchReadback(C.Structure):
     _fields_ = [("a_words", C.POINTER(C.c_uint64)), ("b_words", C.POINTER(C.c_uint64)), ("out", C.c_void_p),
-                ("kernel_ns", C.POINTER(C.c_double)), ("stream_ns", C.POINTER(C.c_double))]
+                ("kernel_ns", C.POINTER(C.c_double)), ("stream_ns", C.POINTER(C.c_double)),
+                ("graph_ns", C.POINTER(C.c_double))]
 
 
 class LayerSpec(C.Structure):

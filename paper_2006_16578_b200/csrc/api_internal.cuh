@@ -73,5 +73,10 @@ void tc_prepare_filter(const ConvShape& s, const uint64_t* filt_plain, TcFilter&
 bool launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st);
 // Records a tensor-core first-layer launch for btnn_cuda_last_tc_launch (kernels_first_tc.cu).
 void note_first_conv_launch(int mode, int tiles, int grid);
+void note_tc_launch(const char* variant, int units, int grid);
+// Kernel-level BMM on packed operands in one tcgen05 kernel (bmm_tc.cu): RowPacked a (M x K),
+// ColPacked b (N x K), K rounded up to 128 bits <= 1536; EPI_I32 (raw / pm1) or EPI_BITS.
+bool bmm_tc_supported(int M, int N, int K);
+void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st);
 
 }  // namespace btnn_gpu

@@ -103,6 +103,35 @@ static double time_stream(int reps, int warmup, cudaStream_t st, F&& fn) {
   return ms * 1e6 / reps;
 }
 
+// Average device time per call of `reps` calls captured back to back in one CUDA graph and
+// replayed (after `warmup` direct calls and one untimed replay).
+template <class F>
+static double time_graph(int reps, int warmup, cudaStream_t st, F&& fn) {
+  for (int i = 0; i < warmup; ++i) fn();
+  BT_CUDA(cudaStreamSynchronize(st));
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  BT_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < reps; ++i) fn();
+  BT_CUDA(cudaStreamEndCapture(st, &graph));
+  BT_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  BT_CUDA(cudaGraphLaunch(exec, st));
+  cudaEvent_t a, b;
+  BT_CUDA(cudaEventCreate(&a));
+  BT_CUDA(cudaEventCreate(&b));
+  BT_CUDA(cudaEventRecord(a, st));
+  BT_CUDA(cudaGraphLaunch(exec, st));
+  BT_CUDA(cudaEventRecord(b, st));
+  BT_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  BT_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaGraphExecDestroy(exec);
+  cudaGraphDestroy(graph);
+  return ms * 1e6 / reps;
+}
+
 }  // namespace btnn_gpu
 
 using namespace btnn_gpu;
@@ -168,12 +197,19 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
       e.out_i32 = out_i.get<int32_t>();
     }
     TcFilter tcf;
-    const bool tc = engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e);
+    const bool packed = engine_override() != BTNN_ENGINE_POPC && bmm_tc_supported((int)n, (int)n, (int)n);
+    const bool tc = !packed && engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e);
     if (tc) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
     const char* used = "popc";
-    // the whole bmm_pm1 / bmm_pm1_bin call from packed operands: B is an input of the call,
-    // so its tensor-core operand is re-expanded every time
+    // the whole bmm_pm1 / bmm_pm1_bin call from packed operands: one kernel that expands both
+    // operands on chip (bmm_tc.cu) when K fits it; else B's tensor-core operand is re-expanded
+    // every call and the implicit GEMM runs
     auto step = [&] {
+      if (packed) {
+        launch_bmm_tc((int)n, (int)n, (int)n, a.get<uint64_t>(), b.get<uint64_t>(), e, st);
+        used = "tc_i8";
+        return;
+      }
       if (tc) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
       used = launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
     };
@@ -183,10 +219,12 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
     // stream of calls sees it; the per-call median above also pays each call's host launch):
     // the GEMM alone with B prepared, and the whole call.
     if (rb && rb->kernel_ns)
-      *rb->kernel_ns = time_stream(reps, warmup, st, [&] {
-        launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
+      *rb->kernel_ns = time_graph(reps, warmup, st, [&] {
+        if (packed) launch_bmm_tc((int)n, (int)n, (int)n, a.get<uint64_t>(), b.get<uint64_t>(), e, st);
+        else launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
       });
     if (rb && rb->stream_ns) *rb->stream_ns = time_stream(reps, warmup, st, step);
+    if (rb && rb->graph_ns) *rb->graph_ns = time_graph(reps, warmup, st, step);
     if (rb) {
       BT_CUDA(cudaStreamSynchronize(st));
       if (rb->a_words) BT_CUDA(cudaMemcpy(rb->a_words, a.get(), a.bytes(), cudaMemcpyDeviceToHost));

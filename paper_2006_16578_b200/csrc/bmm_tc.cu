@@ -1,0 +1,321 @@
+// bmm_tc.cu — kernel-level BMM on packed operands (bmm_pm1 / bmm_raw / bmm_pm1_bin,
+// bmm.hpp:204-274) as one tcgen05 kernel per call: no pre-expanded operand in HBM, no
+// second launch.
+//
+// One CTA (16 warps) per 128 x 64 output tile (M rows of A, N columns of B), the whole inner
+// dimension at once (Kp = K rounded up to 128 bits, <= 1536):
+//   * B's 64 packed columns (Kp/8 bytes each, contiguous in ColPacked) are expanded to +-1
+//     int8 straight into shared memory in the UMMA K-major canonical layout (8-row x 16-byte
+//     core matrices, LBO 128 B, SBO Kp*8 B); bits past K expand to 0, so pad bits of A
+//     contribute nothing;
+//   * A's 128 packed rows are expanded by the same PRMT sign replication into TMEM (one row
+//     per TMEM lane, tcgen05.st), so A never touches shared memory;
+//   * one thread issues the Kp/32 tcgen05.mma kind::i8 (A from TMEM, B from smem,
+//     M128 x N64 x K32, s32 accumulate into 64 TMEM columns) and commits to an mbarrier;
+//   * the epilogue reads the exact +-1 dot v = K - 2 popc(a ^ b) per (row, column) and
+//     writes int32 v (bmm_pm1), (K - v) / 2 = popc (bmm_raw) or the thresholded bit
+//     (lo <= v <= hi, bmm_pm1_bin) packed into RowPacked output words.
+// Both operands use the same K permutation (pm1.cuh), so the dot products are exact.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "api_internal.cuh"
+#include "kernels.cuh"
+#include "pm1.cuh"
+#include "umma.cuh"
+
+namespace btnn_gpu {
+
+namespace bmmtc {
+constexpr int kThreads = 512;
+constexpr int kBM = 128, kBN = 64;
+constexpr int kMaxKp = 1536;  // A in TMEM: Kp/4 columns + 64 accumulator columns <= 512
+}  // namespace bmmtc
+
+struct BmmTcArgs {
+  const uint64_t* a;  // RowPacked M x Kp bits
+  const uint64_t* b;  // ColPacked N x Kp bits
+  int M, N, K, Kp;
+  int mode;                // EPI_I32 (raw or pm1) or EPI_BITS
+  int raw;                 // EPI_I32: (K - v) / 2
+  int32_t* out;            // M x N int32
+  uint32_t* out_bits;      // RowPacked M x (cwo * 64) bits, as 32-bit words
+  int cwo32;               // output words (32-bit) per row
+  const long long* thr_lo;  // EPI_BITS: per column lo / hi (nullptr: v >= 0)
+  const long long* thr_hi;
+};
+
+// Staging slot of 16-byte chunk c of packed row r (cpr chunks per row): c ^ (r & 7) when that
+// stays inside the row (every power-of-two cpr >= 8 and any cpr for the chunks it maps), else c.
+// The map is a bijection on [0, cpr): x = c ^ (r & 7) < cpr is taken only when it is, and
+// pairs (c, x) swap; chunks whose partner is out of range keep their slot.
+__device__ __forceinline__ int stage_slot(int r, int c, int cpr) {
+  const int x = c ^ (r & 7);
+  return x < cpr ? x : c;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+bool bmm_tc_supported(int M, int N, int K) {
+  const int kp = (K + 127) / 128 * 128;
+  return M >= 1 && N >= 1 && K >= 1 && kp <= bmmtc::kMaxKp;
+}
+
+// Timing experiments (BTNN_TIMING builds): clock64 phase stamps of CTA 0, thread 0.
+__device__ unsigned long long g_bmm_ts[16];
+__device__ unsigned long long g_bmm_cta[2 * 1024];  // per CTA: globaltimer at start / end
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define BMM_STAMP(k) \
+  if (BTNN_TIMING && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_bmm_ts[k] = clock64();
+
+__global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid_constant__ BmmTcArgs p) {
+  using namespace umma;
+  BMM_STAMP(0)
+  const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+  if (BTNN_TIMING && threadIdx.x == 0 && cta < 1024) g_bmm_cta[2 * cta] = gtimer();
+  extern __shared__ __align__(1024) uint8_t smem[];  // B: 64 rows x Kp bytes, canonical K-major
+  __shared__ uint64_t mma_done;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int2 thr[bmmtc::kBN];  // EPI_BITS: per column (lo, width) of the range test
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, part = warp >> 2;  // TMEM lane quarter, and which quarter of the work
+  const int m0 = blockIdx.y * bmmtc::kBM, n0 = blockIdx.x * bmmtc::kBN;
+  const int Kp = p.Kp;
+  const uint32_t sbo = (uint32_t)Kp * 8;
+  // Stage the packed tiles in shared memory with coalesced 16-byte cp.async (consecutive lanes
+  // on consecutive 16-byte chunks of a row / column; rows of A and columns of B are contiguous
+  // in RowPacked / ColPacked), issued first so their latency covers the setup below. Chunk c of
+  // row r lands at slot stage_slot(r, c), so the per-row reads (one row per lane) are
+  // bank-conflict-free.
+  const int cpr = Kp / 128;  // 16-byte chunks per packed row
+  uint8_t* a_stage = smem + (size_t)bmmtc::kBN * Kp;          // 128 rows x Kp/8 bytes
+  uint8_t* b_stage = a_stage + (size_t)bmmtc::kBM * (Kp / 8);  // 64 columns x Kp/8 bytes
+  {
+    const uint8_t* ga = reinterpret_cast<const uint8_t*>(p.a);
+    const uint8_t* gb = reinterpret_cast<const uint8_t*>(p.b);
+    for (int g = tid; g < bmmtc::kBM * cpr; g += bmmtc::kThreads) {
+      const int r = g / cpr, c = g - r * cpr, row = m0 + r;
+      const bool ok = row < p.M;
+      cp_async16(smem_u32(a_stage + (size_t)r * (Kp / 8) + (size_t)stage_slot(r, c, cpr) * 16),
+                 ga + ((size_t)(ok ? row : 0) * cpr + c) * 16, ok ? 16 : 0);
+    }
+    for (int g = tid; g < bmmtc::kBN * cpr; g += bmmtc::kThreads) {
+      const int r = g / cpr, c = g - r * cpr, col = n0 + r;
+      const bool ok = col < p.N;
+      cp_async16(smem_u32(b_stage + (size_t)r * (Kp / 8) + (size_t)stage_slot(r, c, cpr) * 16),
+                 gb + ((size_t)(ok ? col : 0) * cpr + c) * 16, ok ? 16 : 0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  if (tid == 0) {
+    mbar_init(&mma_done, 1);
+    fence_mbar_init();
+  }
+  if (p.mode == EPI_BITS && tid < bmmtc::kBN) {
+    // (v - lo) <= width in 32 bits, bounds clamped to +-2^30 (|v| <= K < 2^30); an empty
+    // range never fires; no thresholds: v >= 0
+    int lo32 = 0;
+    uint32_t w = 1u << 30;
+    const int n = min(n0 + tid, p.N - 1);
+    if (p.thr_lo) {
+      const long long l = p.thr_lo[n], h = p.thr_hi[n];
+      const long long lc = l < -(1ll << 30) ? -(1ll << 30) : l, hc = h > (1ll << 30) ? (1ll << 30) : h;
+      lo32 = lc > hc ? (1 << 30) + 1 : (int)lc;
+      w = lc > hc ? 0u : (uint32_t)(hc - lc);
+    }
+    thr[tid] = make_int2(lo32, (int)w);
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  BMM_STAMP(1)
+  // Warp 0 allocates TMEM while warps 1-15 expand B: it only arrives (bar.arrive) on the
+  // staging barrier, whose other 15 warps wait (bar.sync) for every thread's copies.
+  if (warp == 0) {
+    asm volatile("bar.arrive 1, %0;" ::"n"(bmmtc::kThreads) : "memory");
+    tmem_alloc(&tmem_base_sh, 512);
+    BMM_STAMP(2)
+  } else {
+    asm volatile("bar.sync 1, %0;" ::"n"(bmmtc::kThreads) : "memory");
+    // ---- B -> +-1 bytes (0 past K) in shared memory, canonical K-major ----
+    // item = (column n, chunk c): lanes on consecutive columns (n & 7 spans one core-matrix
+    // row group: the 16-byte stores of 8 lanes cover all 32 banks)
+    for (int g = tid - 32; g < bmmtc::kBN * cpr; g += bmmtc::kThreads - 32) {
+      const int n = g & 63, c = g >> 6;
+      const uint4 bits = *reinterpret_cast<const uint4*>(b_stage + (size_t)n * (Kp / 8) + stage_slot(n, c, cpr) * 16);
+      const uint32_t w4[4] = {bits.x, bits.y, bits.z, bits.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = 4 * c + u;       // 32-bit word of the column
+        const int rem = p.K - 32 * i;  // valid bits of this word
+        uint32_t o[8];
+        if (n0 + n < p.N && rem > 0) {
+          expand_word(w4[u], o);
+          if (rem < 32) {
+            // byte k of word s holds bit 8k + 7 - s: zero the bytes of bits >= rem
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              uint32_t keep = 0;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) keep |= (8 * k + 7 - s < rem ? 0xFFu : 0u) << (8 * k);
+              o[s] &= keep;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < 8; ++s) o[s] = 0u;
+        }
+        // K index 32i + 4s + k: core-matrix column 2i (s < 4) and 2i + 1 (s >= 4)
+        uint8_t* dst = smem + (size_t)(n >> 3) * sbo + (size_t)(2 * i) * 128 + (n & 7) * 16;
+        *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(dst + 128) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();  // the TMEM base is visible
+  fence_after();
+  BMM_STAMP(3)
+  const uint32_t tbase = tmem_base_sh;
+  const uint32_t a_col0 = bmmtc::kBN;  // A after the 64 accumulator columns
+  // ---- A -> +-1 bytes in TMEM, one row per lane; warp: lane quarter q, chunks c = part mod 4 ----
+  {
+    const int r = q * 32 + lane;
+    const uint8_t* arow = a_stage + (size_t)r * (Kp / 8);
+    for (int c = part; c < cpr; c += 4) {
+      const uint4 bits = *reinterpret_cast<const uint4*>(arow + stage_slot(r, c, cpr) * 16);
+      uint32_t v[32];
+      expand_word(bits.x, v);
+      expand_word(bits.y, v + 8);
+      expand_word(bits.z, v + 16);
+      expand_word(bits.w, v + 24);
+      tmem_st32(taddr(tbase, q * 32, a_col0 + 32 * c), v);
+    }
+    tmem_st_wait();
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B read by the tensor core
+  fence_before();
+  __syncthreads();
+  fence_after();
+  BMM_STAMP(4)
+  if (tid == 0) {
+    // one thread, descriptors advanced by their start-address field (16-byte units)
+    const uint32_t idesc = idesc_i8(bmmtc::kBM, bmmtc::kBN);
+    const uint64_t b0 = sdesc(smem_u32(smem), 128, sbo);
+    for (int j = 0; j < Kp / 32; ++j) mma_i8_ts(tbase, tbase + a_col0 + 8 * j, b0 + (uint64_t)(16 * j), idesc, j > 0);
+    mma_commit(&mma_done);
+  }
+  BMM_STAMP(5)
+  mbar_wait(&mma_done, 0);
+  fence_after();
+  BMM_STAMP(6)
+  // ---- epilogue: warp (q, part) reads lane quarter q, columns part * 16 .. + 15 ----
+  {
+    const int r = q * 32 + lane, row = m0 + r, c0 = part * 16;
+    uint32_t acc[16];
+    tmem_ld16(taddr(tbase, q * 32, c0), acc);
+    tmem_ld_wait();
+    const int ncol = min(16, p.N - (n0 + c0));
+    if (p.mode == EPI_BITS) {
+      if (row < p.M && ncol > 0) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int2 t = thr[c0 + j];
+          word |= (uint32_t)((uint32_t)((int)acc[j] - t.x) <= (uint32_t)t.y) << j;
+        }
+        if (ncol < 16) word &= (1u << ncol) - 1u;
+        reinterpret_cast<uint16_t*>(p.out_bits)[(size_t)row * p.cwo32 * 2 + (n0 + c0) / 16] = (uint16_t)word;
+      }
+    } else {
+      // through shared memory (B's expanded tile is dead once the MMAs completed): rows of 64
+      // int32 at a 272-byte pitch (16-byte stores of consecutive rows hit different banks),
+      // then each warp instruction writes two full 256-byte output row segments
+      constexpr int kPitch = 68;  // int32 per staged row
+      int32_t* st = reinterpret_cast<int32_t*>(smem);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        int4 v;
+        v.x = p.raw ? (p.K - (int)acc[j]) / 2 : (int)acc[j];
+        v.y = p.raw ? (p.K - (int)acc[j + 1]) / 2 : (int)acc[j + 1];
+        v.z = p.raw ? (p.K - (int)acc[j + 2]) / 2 : (int)acc[j + 2];
+        v.w = p.raw ? (p.K - (int)acc[j + 3]) / 2 : (int)acc[j + 3];
+        *reinterpret_cast<int4*>(st + r * kPitch + c0 + j) = v;
+      }
+      __syncthreads();
+      const bool vec = (p.N & 3) == 0 && n0 + bmmtc::kBN <= p.N;
+      for (int rr = warp * 2 + (lane >> 4); rr < bmmtc::kBM; rr += 2 * (bmmtc::kThreads / 32)) {
+        const int orow = m0 + rr;
+        if (orow >= p.M) break;
+        const int cc = (lane & 15) * 4;
+        int32_t* dst = p.out + (size_t)orow * p.N + n0 + cc;
+        const int4 v = *reinterpret_cast<const int4*>(st + rr * kPitch + cc);
+        if (vec) {
+          *reinterpret_cast<int4*>(dst) = v;
+        } else {
+          const int vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (n0 + cc + k < p.N) dst[k] = vv[k];
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  BMM_STAMP(7)
+  if (warp == 0) tmem_dealloc(tbase, 512);
+  BMM_STAMP(8)
+  if (BTNN_TIMING && threadIdx.x == 0 && cta < 1024) g_bmm_cta[2 * cta + 1] = gtimer();
+}
+
+// act: RowPacked M x K (stride ru(K, 128) bits), filt: ColPacked N x K; the Epi carries the
+// output (EPI_I32 raw / pm1 into out_i32, EPI_BITS into out_bits with optional thresholds).
+void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
+  BmmTcArgs p{};
+  p.a = a;
+  p.b = b;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Kp = (K + 127) / 128 * 128;
+  p.mode = e.mode;
+  p.raw = e.raw;
+  p.out = e.out_i32;
+  p.out_bits = reinterpret_cast<uint32_t*>(e.out_bits);
+  p.cwo32 = (N + 127) / 128 * 4;
+  p.thr_lo = e.thr_lo;
+  p.thr_hi = e.thr_hi;
+  // One CTA per SM: each allocates all 512 TMEM columns, so a second co-resident CTA would
+  // block in tcgen05.alloc until the first exits — request enough smem that two never fit.
+  const int smem = std::max(bmmtc::kBN * p.Kp + (bmmtc::kBM + bmmtc::kBN) * p.Kp / 8, 120 * 1024);
+  static thread_local int configured = -1;
+  int dev = 0;
+  BT_CUDA(cudaGetDevice(&dev));
+  if (configured != dev) {
+    BT_CUDA(cudaFuncSetAttribute(bmm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 std::max(bmmtc::kBN * bmmtc::kMaxKp + (bmmtc::kBM + bmmtc::kBN) * bmmtc::kMaxKp / 8,
+                                          120 * 1024)));
+    configured = dev;
+  }
+  const dim3 grid((unsigned)((N + bmmtc::kBN - 1) / bmmtc::kBN), (unsigned)((M + bmmtc::kBM - 1) / bmmtc::kBM));
+  bmm_tc_kernel<<<grid, bmmtc::kThreads, smem, st>>>(p);
+  BT_CUDA(cudaGetLastError());
+  note_tc_launch(e.mode == EPI_BITS ? "bmm_packed/bin" : "bmm_packed/i32", (int)(grid.x * grid.y), (int)(grid.x * grid.y));
+}
+
+}  // namespace btnn_gpu
+
+extern "C" int btnn_cuda_debug_bmm_timestamps(unsigned long long* out, size_t n) {
+  return btnn_gpu::guard([&] {
+    BT_CUDA(cudaDeviceSynchronize());
+    BT_CUDA(cudaMemcpyFromSymbol(out, btnn_gpu::g_bmm_ts, (n < 16 ? n : 16) * 8));
+    if (n >= 16 + 2048) BT_CUDA(cudaMemcpyFromSymbol(out + 16, btnn_gpu::g_bmm_cta, 2048 * 8));
+  });
+}

@@ -243,6 +243,16 @@ static const char* run_gemm(const ConvShape& s0, const uint64_t* act, const uint
   return launch_bgemm(s, act, filt, e, st, EngineHint::Auto, tc ? &tcf : nullptr);
 }
 
+// Kernel-level BMM (bmm.hpp:204-274): the one-kernel packed-operand GEMM when the inner
+// dimension fits it (bmm_tc.cu), else the implicit-GEMM path with B expanded for the call.
+static const char* run_bmm(const ConvShape& s, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
+  if (engine_override() != BTNN_ENGINE_POPC && bmm_tc_supported(s.N, s.O, s.C)) {
+    launch_bmm_tc(s.N, s.O, s.C, a, b, e, st);
+    return "tc_i8";
+  }
+  return run_gemm(s, a, b, e, st);
+}
+
 }  // namespace btnn_gpu
 
 using namespace btnn_gpu;
@@ -452,7 +462,7 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
       e.mode = EPI_I32;
       e.raw = which == 0;
       e.out_i32 = o.get<int32_t>();
-      run_gemm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st);
+      run_bmm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st);
       BT_CUDA(cudaMemcpy(out, o.get(), a->rows * b->cols * 4, cudaMemcpyDeviceToHost));
       return;
     }
@@ -468,7 +478,7 @@ static int bmm_entry(int which, const btnn_matrix_desc* a, const uint64_t* aw, c
     BT_CUDA(cudaMemsetAsync(rp.get(), 0, rp.bytes(), st));
     e.mode = EPI_BITS;
     e.out_bits = rp.get<uint64_t>();
-    run_gemm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st);
+    run_bmm(op.s, op.a.get<uint64_t>(), op.b.get<uint64_t>(), e, st);
     const int out_layout = a->layout == BTNN_FSB_ROW ? BTNN_FSB_ROW : BTNN_ROW_PACKED;
     const size_t words = mat_words(a->rows, b->cols, out_layout, a->bh, a->bw);
     if (out_layout == BTNN_ROW_PACKED) {

@@ -68,6 +68,31 @@ def test_bmm_1024_cube():
     assert np.array_equal(1024 - 2 * raw, want)
 
 
+@pytest.mark.parametrize("m,n,k", [(300, 700, 1536), (1000, 65, 1200), (129, 1, 33), (1, 129, 1408), (130, 131, 1537)])
+def test_bmm_packed_kernel_shapes(m, n, k, engine):
+    """The one-kernel packed BMM (bmm_tc.cu) over tile edges in M and N, inner dimensions up to
+    its 1536-bit limit (partial last words, odd chunk counts), and past it (the implicit-GEMM
+    path): pm1, raw and thresholded bits vs the C oracle."""
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    fa, fb = rng.standard_normal(m * k, dtype=np.float32), rng.standard_normal(k * n, dtype=np.float32)
+    A, Bw = Wt.pack_matrix(fa, m, k, capi.ROW_PACKED), Wt.pack_matrix(fb, k, n, capi.COL_PACKED)
+    da, db = md(m, k, capi.ROW_PACKED), md(k, n, capi.COL_PACKED)
+    want = np.zeros(m * n, dtype=np.int32)
+    oracle().bo_bmm_pm1(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64), capi.BMM_NAIVE,
+                        ptr(want, C.c_int32))
+    assert np.array_equal(B.bmm_pm1(da, A, db, Bw).reshape(-1), want), (m, n, k)
+    if engine == "tc":
+        assert capi.last_tc_launch()[0] == ("bmm_packed/i32" if k <= 1536 else "tmemA/i32"), capi.last_tc_launch()
+    if k % 128 == 0:
+        assert np.array_equal(k - 2 * B.bmm_raw(da, A, db, Bw).reshape(-1), want)
+    bits = B.bmm_pm1_bin(da, A, db, Bw)
+    dense = (want.reshape(m, n) >= 0)
+    words = np.zeros((m, (n + 127) // 128 * 2), dtype=np.uint64)
+    for j in range(n):
+        words[:, j // 64] |= dense[:, j].astype(np.uint64) << np.uint64(j % 64)
+    assert np.array_equal(np.asarray(bits).reshape(-1), words.reshape(-1))
+
+
 @pytest.mark.parametrize("i", indices(load("bconv"), "c", "case"))
 def test_bconv_golden(i):
     d = load("bconv")
