@@ -306,6 +306,17 @@ int btnn_cuda_plan_read_tap(btnn_plan* plan, size_t i, size_t batch, double* out
  * 2x2-averaged tap directly (averaged = 1, h = out_h/2, w = out_w/2); otherwise the full
  * tap (averaged = 0). */
 int btnn_cuda_plan_tap_dims(btnn_plan* plan, size_t i, size_t* dims);
+/* Plan tuner (on by default; BTNN_AUTOTUNE=0 or btnn_cuda_set_autotune(0) turns it off for
+ * plans created afterwards): at plan_create every tensor-core conv layer times each
+ * geometry its shape allows (the cost model's pick, halo mode at each feasible sites-per-tile,
+ * the TMEM-A path) in eager forwards at the plan's max batch and keeps the fastest. All
+ * geometries compute the same exact sums. */
+int btnn_cuda_set_autotune(int enabled);
+/* Layer i's candidates as "name,name,..." with the pick starred ("*halo/spt2,halo/spt4,tmemA"),
+ * and their measured ms (n_ms entries at most); "" for layers without candidates. */
+int btnn_cuda_plan_layer_choice(btnn_plan* plan, size_t i, char* buf, size_t n, double* ms, size_t n_ms);
+/* Run candidate k (btnn_cuda_plan_layer_choice order) for layer i from now on. */
+int btnn_cuda_plan_set_layer_choice(btnn_plan* plan, size_t i, size_t k);
 /* Name of the engine chosen for layer i ("tc_i8", "popc", "fp64", "orpool", ...). */
 const char* btnn_cuda_plan_layer_engine(btnn_plan* plan, size_t i);
 int btnn_cuda_plan_destroy(btnn_plan* plan);

@@ -282,6 +282,20 @@ class Plan:
         check(lib().btnn_cuda_plan_read_tap(self.h, i, batch, _p(out, C.c_double)))
         return out
 
+    def layer_choice(self, i: int):
+        """(candidate names, index of the pick, measured ms per candidate) of layer i's tuned
+        tensor-core geometry (empty for layers without candidates)."""
+        buf = C.create_string_buffer(256)
+        ms = (C.c_double * 16)()
+        check(lib().btnn_cuda_plan_layer_choice(self.h, i, buf, 256, ms, 16))
+        names = [n for n in buf.value.decode().split(",") if n]
+        pick = next((k for k, n in enumerate(names) if n.startswith("*")), -1)
+        return [n.lstrip("*") for n in names], pick, list(ms[:len(names)])
+
+    def set_layer_choice(self, i: int, k: int):
+        """Run candidate k of layer_choice(i) for layer i from now on."""
+        check(lib().btnn_cuda_plan_set_layer_choice(self.h, i, k))
+
     def engines(self):
         return [lib().btnn_cuda_plan_layer_engine(self.h, i).decode() for i in range(self.n_layers)]
 

@@ -60,9 +60,20 @@ struct TcFilter {
   bool valid() const { return w8.get() != nullptr; }
 };
 
+// Geometry of one tensor-core launch, chosen per layer shape by measurement (the plan's
+// tuner, plan.cu): spt > 0 runs halo mode with that many output sites per tile, tmem_a = 1
+// the TMEM-A path; {0, 0} is the cost model's choice (kernels_tc.cu tc_geom).
+struct TcChoice {
+  int spt = 0, tmem_a = 0;
+};
+// The distinct feasible geometries of (s, e), the cost model's own first; "halo/sptN" or
+// "tmemA" names them.
+std::vector<TcChoice> tc_choices(const ConvShape& s, const Epi& e);
+std::string tc_choice_name(const ConvShape& s, const Epi& e, const TcChoice& c);
+
 // Returns the engine name used ("tc_i8" / "popc").
 const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e,
-                         cudaStream_t st, EngineHint h, const TcFilter* tc = nullptr);
+                         cudaStream_t st, EngineHint h, const TcFilter* tc = nullptr, const TcChoice* ch = nullptr);
 
 // True when launch_bgemm would pick the tensor-core engine for (s, e).
 bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter* tc);
@@ -70,7 +81,8 @@ bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter*
 // Tensor-core support (kernels_tc.cu).
 bool tc_supported(const ConvShape& s, const Epi& e);
 void tc_prepare_filter(const ConvShape& s, const uint64_t* filt_plain, TcFilter& out, cudaStream_t st);
-bool launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st);
+bool launch_bgemm_tc(const ConvShape& s, const uint64_t* act, const TcFilter& f, const Epi& e, cudaStream_t st,
+                     const TcChoice* ch = nullptr);
 // Records a tensor-core first-layer launch for btnn_cuda_last_tc_launch (kernels_first_tc.cu).
 void note_first_conv_launch(int mode, int tiles, int grid);
 void note_tc_launch(const char* variant, int units, int grid);

@@ -32,14 +32,14 @@ bool will_use_tc(const ConvShape& s, const Epi& e, EngineHint h, const TcFilter*
 }
 
 const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t* filt, const Epi& e, cudaStream_t st,
-                         EngineHint h, const TcFilter* tc) {
+                         EngineHint h, const TcFilter* tc, const TcChoice* ch) {
   h = resolve(h);
   const bool tc_ok = tc && tc->valid() && tc_supported(s, e);
   if (h == EngineHint::TcI8) require(tc_ok, BTNN_UNSUPPORTED_SHAPE, "tensor-core engine does not cover this shape");
   require(e.rout_half == nullptr || (tc_ok && h != EngineHint::Popc), BTNN_CUDA_ERROR,
           "halved tap output needs the tensor-core engine");
   if (tc_ok && h != EngineHint::Popc) {
-    return launch_bgemm_tc(s, act, *tc, e, st) ? "tc_i8_splitk" : "tc_i8";
+    return launch_bgemm_tc(s, act, *tc, e, st, ch) ? "tc_i8_splitk" : "tc_i8";
   }
   launch_bgemm_popc(s, act, filt, e, st);
   return "popc";

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <cstdlib>
 #include <map>
@@ -46,6 +47,12 @@ struct LayerDev {
   bool halo_ok = false;                         // conv may run the halo-mode kernel (filter layout)
   bool pool_fused = false;                      // or_pool layer folded into the previous conv's epilogue
   std::string engine = "-";
+  // Measured geometry choice (tune_shard): the candidates of the layer's shape, their
+  // measured ms at the shard's max batch, and the pick.
+  TcChoice choice;
+  std::vector<TcChoice> cands;
+  std::vector<std::string> cand_names;
+  std::vector<double> cand_ms;
 };
 
 struct Shard {
@@ -68,6 +75,7 @@ struct Shard {
   cudaStream_t copy_stream = nullptr;    // host->device input chunks (run_shard_host)
   std::vector<cudaEvent_t> in_ready;     // per chunk: input resident
   size_t launches = 0;
+  int tune_pass = -1;  // >= 0 while tune_shard runs candidate pass k of every layer
   ~Shard() {
     if (device >= 0) cudaSetDevice(device);
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
@@ -406,7 +414,15 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h / e.pool, l.out_w / e.pool, batch, l.out_channels, 0, 0, 0) * 8, st));
       else if (!(tc && np == batch))
         BT_CUDA(cudaMemsetAsync(out, 0, act_words(l.out_h, l.out_w, batch, l.out_channels, 0, 0, 0) * 8, st));
-      L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
+      if (sh.tune_pass >= 0 && tc) {  // plan tuner: this pass's candidate geometry
+        if (L.cands.empty()) {
+          L.cands = tc_choices(s, e);
+          for (const TcChoice& c : L.cands) L.cand_names.push_back(tc_choice_name(s, e, c));
+          L.cand_ms.assign(L.cands.size(), 0.0);
+        }
+        L.choice = L.cands[std::min((size_t)sh.tune_pass, L.cands.size() - 1)];
+      }
+      L.engine = launch_bgemm(s, in, L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc, &L.choice);
       if (e.pool) L.engine += "+pool";
       ++launches;
       cur ^= 1;
@@ -578,6 +594,89 @@ using namespace btnn_gpu;
 
 extern "C" {
 
+namespace btnn_gpu {
+// Plan tuner (north star (2): the variant per layer shape from measured throughput). Every
+// tensor-core conv layer lists the distinct geometries its shape allows (tc_choices: the cost
+// model's pick, halo mode at each feasible sites-per-tile, the TMEM-A path); pass k runs
+// candidate k of every layer in one eager forward at the shard's max batch (an all-zero
+// input) with per-layer events, twice (the first warms up), and each layer keeps its fastest.
+// Every candidate computes the same exact sums, so the pick changes speed only.
+static std::atomic<int> g_autotune{[] {
+  const char* v = std::getenv("BTNN_AUTOTUNE");
+  return v ? std::atoi(v) : 1;
+}()};
+
+static void tune_shard(btnn_plan* plan, Shard& sh) {
+  BT_CUDA(cudaSetDevice(sh.device));
+  const size_t B = sh.max_batch;
+  BT_CUDA(cudaMemsetAsync(sh.x.get(), 0, sh.x.bytes(), sh.stream));
+  size_t passes = 1;
+  for (size_t pass = 0; pass < passes; ++pass) {
+    sh.tune_pass = (int)pass;
+    for (int rep = 0; rep < 2; ++rep) {
+      BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
+      enqueue_forward(plan, sh, sh.x.get<float>(), B, sh.logits.get<double>(), sh.labels.get<int32_t>(), true);
+    }
+    BT_CUDA(cudaStreamSynchronize(sh.stream));
+    for (size_t i = 0; i < sh.layers.size(); ++i) {
+      LayerDev& L = sh.layers[i];
+      passes = std::max(passes, L.cands.size());
+      if (pass < L.cands.size()) {
+        float ms = 0.f;
+        BT_CUDA(cudaEventElapsedTime(&ms, sh.events[i], sh.events[i + 1]));
+        L.cand_ms[pass] = ms;
+      }
+    }
+  }
+  sh.tune_pass = -1;
+  for (LayerDev& L : sh.layers) {
+    if (L.cands.empty()) continue;
+    size_t best = 0;
+    for (size_t k = 1; k < L.cands.size(); ++k)
+      if (L.cand_ms[k] < L.cand_ms[best]) best = k;
+    L.choice = L.cands[best];
+  }
+}
+}  // namespace btnn_gpu
+
+int btnn_cuda_set_autotune(int enabled) {
+  return guard([&] { g_autotune.store(enabled != 0); });
+}
+
+int btnn_cuda_plan_layer_choice(btnn_plan* plan, size_t i, char* buf, size_t n, double* ms, size_t n_ms) {
+  return guard([&] {
+    require(plan && !plan->shards.empty() && i < plan->specs.size(), BTNN_INVALID_INPUT, "plan_layer_choice: bad layer");
+    const LayerDev& L = plan->shards[0]->layers[i];
+    std::string out;
+    size_t pick = 0;
+    for (size_t k = 0; k < L.cands.size(); ++k)
+      if (L.cands[k].spt == L.choice.spt && L.cands[k].tmem_a == L.choice.tmem_a) pick = k;
+    for (size_t k = 0; k < L.cands.size(); ++k) {
+      out += (k ? "," : "") + std::string(k == pick ? "*" : "") + L.cand_names[k];
+      if (ms && k < n_ms) ms[k] = L.cand_ms[k];
+    }
+    if (buf && n) {
+      const size_t c = std::min(n - 1, out.size());
+      std::memcpy(buf, out.data(), c);
+      buf[c] = 0;
+    }
+  });
+}
+
+int btnn_cuda_plan_set_layer_choice(btnn_plan* plan, size_t i, size_t k) {
+  return guard([&] {
+    require(plan && !plan->shards.empty() && i < plan->specs.size(), BTNN_INVALID_INPUT, "plan_set_layer_choice: bad layer");
+    for (auto& sh : plan->shards) {
+      LayerDev& L = sh->layers[i];
+      require(k < L.cands.size(), BTNN_INVALID_INPUT, "plan_set_layer_choice: no such candidate");
+      L.choice = L.cands[k];
+      BT_CUDA(cudaSetDevice(sh->device));
+      for (auto& kv : sh->graphs) cudaGraphExecDestroy(kv.second.exec);  // captured with the old choice
+      sh->graphs.clear();
+    }
+  });
+}
+
 int btnn_cuda_plan_create(const btnn_model_spec* m, const btnn_weight_store* ws, size_t max_batch, const int* devices,
                           int n_devices, btnn_plan** out) {
   return guard([&] {
@@ -605,6 +704,8 @@ int btnn_cuda_plan_create(const btnn_model_spec* m, const btnn_weight_store* ws,
       build_shard(*sh, m, ws);
       plan->shards.push_back(std::move(sh));
     }
+    if (g_autotune.load())
+      for (auto& sh : plan->shards) tune_shard(plan.get(), *sh);
     *out = plan.release();
   });
 }

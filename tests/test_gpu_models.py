@@ -168,3 +168,52 @@ def test_uncleared_outputs_pad_words(batch):
         want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
         assert np.array_equal(lg.view(np.uint64), want.view(np.uint64)), plan.engines()
         assert np.array_equal(lb, wl)
+
+
+def test_plan_tuner_measured_choices(engine):
+    """The plan tuner (north star (2)): every tensor-core conv layer of a residual model lists
+    its feasible geometries with measured times and runs the fastest; tuned and untuned plans
+    both equal the oracle bit for bit."""
+    m = M.make_model("tune", "64C3-64C3-64C3-128C3/2-128C3-128C3-10FC", 28, 28, 3, 10, [(0, 2), (2, 5)])
+    ws = Wt.build_weights(m, Wt.random_weights(m, 77))
+    x = np.random.default_rng(78).standard_normal((40, 28, 28, 3), dtype=np.float32)
+    want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+    try:
+        capi.lib().btnn_cuda_set_autotune(0)
+        plain = B.Plan(m, ws, 40)
+    finally:
+        capi.lib().btnn_cuda_set_autotune(1)
+    tuned = B.Plan(m, ws, 40)
+    for plan in (plain, tuned):
+        lg, lb = plan.run(x)
+        assert np.array_equal(lg.view(np.uint64), want.view(np.uint64)) and np.array_equal(lb, wl)
+    tc_layers = [i for i, e in enumerate(tuned.engines()) if e.startswith("tc_i8") and i > 0]
+    if engine == "popc":
+        assert not tc_layers
+        return
+    assert tc_layers
+    multi = 0
+    for i in tc_layers:
+        names, pick, ms = tuned.layer_choice(i)
+        if m.layers[i].kind == capi.BIT_CONV:
+            assert names and 0 <= pick < len(names) and all(t > 0 for t in ms), (i, names, ms)
+            assert ms[pick] == min(ms)
+            multi += len(names) > 1
+        assert plain.layer_choice(i)[0] == []  # untuned: the cost model, no candidates measured
+    assert multi >= 1
+
+
+@pytest.mark.parametrize("prefix,fm", fixture_models(), ids=lambda v: v if isinstance(v, str) else "")
+def test_every_tuner_candidate_bit_exact(prefix, fm, engine):
+    """Each geometry the tuner may pick, forced layer by layer, equals the reference."""
+    if engine == "popc":
+        return
+    plan = B.Plan(fm.spec, fm.store, fm.x.shape[0])
+    for i in range(fm.spec.n_layers):
+        names, pick, _ = plan.layer_choice(i)
+        for k in range(len(names)):
+            plan.set_layer_choice(i, k)
+            lg, lb = plan.run(fm.x)
+            assert np.array_equal(lg.view(np.uint64), fm.logits.view(np.uint64)), (i, names[k], plan.engines())
+        if names:
+            plan.set_layer_choice(i, pick)
