@@ -218,6 +218,14 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
 int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
                           double* median_ns, double* min_ns, char* engine, size_t engine_len,
                           const btnn_bench_readback* rb);
+/* The same suites on fsb-layout operands (8 x 128 tiles; the reference's "fsb" rows,
+ * bench.hpp:140-156, 230-245): the tiled operands are converted on the device inside every
+ * timed call (and a bit result back to tiles). Readback buffers receive the plain forms. */
+int btnn_cuda_bench_bmm_fsb(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
+                            size_t engine_len, const btnn_bench_readback* rb);
+int btnn_cuda_bench_bconv_fsb(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps,
+                              int warmup, double* median_ns, double* min_ns, char* engine, size_t engine_len,
+                              const btnn_bench_readback* rb);
 
 /* ---- model driver (inference.hpp:67-186) ----------------------------------------- */
 /* LayerSpec (model.hpp:36-52), already resolved (resolve_model, model.hpp:190-296). */

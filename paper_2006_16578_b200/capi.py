@@ -119,7 +119,10 @@ _PROTOS = {
     "btnn_cuda_first_conv_bwn": (C.c_int, [f32p, sz, sz, sz, sz, f32p, sz, sz, sz, sz, P(ConvGeom), f64p]),
     "btnn_cuda_or_pool": (C.c_int, [P(ActDesc), u64p, sz, sz, u64p]),
     "btnn_cuda_bench_bmm": (C.c_int, [sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz, P(BenchReadback)]),
+    "btnn_cuda_bench_bmm_fsb": (C.c_int, [sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz, P(BenchReadback)]),
     "btnn_cuda_bench_bconv": (C.c_int, [sz, sz, sz, sz, sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz,
+                                        P(BenchReadback)]),
+    "btnn_cuda_bench_bconv_fsb": (C.c_int, [sz, sz, sz, sz, sz, C.c_int, C.c_int, C.c_int, f64p, f64p, C.c_char_p, sz,
                                         P(BenchReadback)]),
     "btnn_cuda_plan_create": (C.c_int, [P(ModelSpec), P(WeightStore), sz, P(C.c_int), C.c_int, P(C.c_void_p)]),
     "btnn_cuda_plan_run": (C.c_int, [C.c_void_p, f32p, sz, f64p, i32p]),

@@ -161,8 +161,8 @@ int btnn_cuda_selftest_div(const double* a, const double* b, size_t n, double* f
 }
 
 
-int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
-                        size_t engine_len, const btnn_bench_readback* rb) {
+static int bench_bmm_impl(size_t n, int bin, int fsb, int reps, int warmup, double* median_ns, double* min_ns,
+                          char* engine, size_t engine_len, const btnn_bench_readback* rb) {
   return guard([&] {
     require(n > 0, BTNN_INVALID_INPUT, "bench_bmm: zero size");
     int dev = 0;
@@ -196,6 +196,31 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
       e.mode = EPI_I32;
       e.out_i32 = out_i.get<int32_t>();
     }
+    // fsb layout (the reference's "fsb" rows, bench.hpp:140-156): the call's operands are FSB
+    // tiles (8 x 128), converted to RowPacked / ColPacked on the device inside every timed
+    // call, and a bit result converted back to FSB rows
+    constexpr size_t kBh = 8, kBw = 128;
+    DevBuf af, bf, tmp_a, tmp_b, of;
+    if (fsb) {
+      af.alloc(mat_words(n, n, BTNN_FSB_ROW, kBh, kBw) * 8);
+      bf.alloc(mat_words(n, n, BTNN_FSB_COL, kBh, kBw) * 8);
+      tmp_a.alloc(a.bytes());
+      tmp_b.alloc(b.bytes());
+      launch_convert_matrix(n, n, BTNN_ROW_PACKED, 0, 0, a.get<uint64_t>(), BTNN_FSB_ROW, kBh, kBw, af.get<uint64_t>(), st);
+      launch_convert_matrix(n, n, BTNN_COL_PACKED, 0, 0, b.get<uint64_t>(), BTNN_FSB_COL, kBh, kBw, bf.get<uint64_t>(), st);
+      if (bin) of.alloc(mat_words(n, n, BTNN_FSB_ROW, kBh, kBw) * 8);
+    }
+    const uint64_t* opa = fsb ? tmp_a.get<uint64_t>() : a.get<uint64_t>();
+    const uint64_t* opb = fsb ? tmp_b.get<uint64_t>() : b.get<uint64_t>();
+    auto to_plain = [&] {
+      if (!fsb) return;
+      launch_convert_matrix(n, n, BTNN_FSB_ROW, kBh, kBw, af.get<uint64_t>(), BTNN_ROW_PACKED, 0, 0, tmp_a.get<uint64_t>(), st);
+      launch_convert_matrix(n, n, BTNN_FSB_COL, kBh, kBw, bf.get<uint64_t>(), BTNN_COL_PACKED, 0, 0, tmp_b.get<uint64_t>(), st);
+    };
+    auto to_fsb_out = [&] {
+      if (fsb && bin)
+        launch_convert_matrix(n, n, BTNN_ROW_PACKED, 0, 0, out_b.get<uint64_t>(), BTNN_FSB_ROW, kBh, kBw, of.get<uint64_t>(), st);
+    };
     TcFilter tcf;
     const bool packed = engine_override() != BTNN_ENGINE_POPC && bmm_tc_supported((int)n, (int)n, (int)n);
     const bool tc = !packed && engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e);
@@ -205,13 +230,15 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
     // operands on chip (bmm_tc.cu) when K fits it; else B's tensor-core operand is re-expanded
     // every call and the implicit GEMM runs
     auto step = [&] {
+      to_plain();
       if (packed) {
-        launch_bmm_tc((int)n, (int)n, (int)n, a.get<uint64_t>(), b.get<uint64_t>(), e, st);
+        launch_bmm_tc((int)n, (int)n, (int)n, opa, opb, e, st);
         used = "tc_i8";
-        return;
+      } else {
+        if (tc) tc_prepare_filter(s, opb, tcf, st);
+        used = launch_bgemm(s, opa, opb, e, st, EngineHint::Auto, &tcf);
       }
-      if (tc) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
-      used = launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
+      to_fsb_out();
     };
     BT_CUDA(cudaStreamSynchronize(st));
     time_reps(reps, warmup, st, step, median_ns, min_ns);
@@ -220,8 +247,8 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
     // the GEMM alone with B prepared, and the whole call.
     if (rb && rb->kernel_ns)
       *rb->kernel_ns = time_graph(reps, warmup, st, [&] {
-        if (packed) launch_bmm_tc((int)n, (int)n, (int)n, a.get<uint64_t>(), b.get<uint64_t>(), e, st);
-        else launch_bgemm(s, a.get<uint64_t>(), b.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
+        if (packed) launch_bmm_tc((int)n, (int)n, (int)n, opa, opb, e, st);
+        else launch_bgemm(s, opa, opb, e, st, EngineHint::Auto, &tcf);
       });
     if (rb && rb->stream_ns) *rb->stream_ns = time_stream(reps, warmup, st, step);
     if (rb && rb->graph_ns) *rb->graph_ns = time_graph(reps, warmup, st, step);
@@ -239,9 +266,9 @@ int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_
   });
 }
 
-int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
-                          double* median_ns, double* min_ns, char* engine, size_t engine_len,
-                          const btnn_bench_readback* rb) {
+static int bench_bconv_impl(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int fsb, int reps,
+                            int warmup, double* median_ns, double* min_ns, char* engine, size_t engine_len,
+                            const btnn_bench_readback* rb) {
   return guard([&] {
     require(input_hw && batch && c && o && k, BTNN_INVALID_INPUT, "bench_bconv: zero size");
     cudaStream_t st;
@@ -297,13 +324,34 @@ int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, siz
     TcFilter tcf;
     if (engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e)) tc_prepare_filter(s, filt.get<uint64_t>(), tcf, st);
     const char* used = "popc";
+    // fsb layout (bench.hpp:230-245): the call's input is the tiled activation tensor
+    // (convert_activations, 8 x 128 tiles), converted to plain HWNC on the device every call;
+    // a bit output goes back to tiles. (The filter is a layer constant: converted and expanded
+    // once, as in the plain rows.)
+    constexpr size_t kBh = 8, kBw = 128;
+    DevBuf in_t, out_t;
+    if (fsb) {
+      in_t.alloc(act_words(H, H, batch, c, 1, kBh, kBw) * 8);
+      if (bin) {
+        launch_convert_act(H, H, batch, c, 0, 0, 0, in.get<uint64_t>(), 1, kBh, kBw, in_t.get<uint64_t>(), st);
+        out_t.alloc(act_words(P, P, batch, o, 1, kBh, kBw) * 8);
+      }
+    }
     auto step = [&] {
       if (!bin) {
         BT_CUDA(cudaMemsetAsync(in.get(), 0, in.bytes(), st));
         launch_pack_nhwc(x.get<float>(), (int)batch, (int)H, (int)H, (int)c, (int)np, (int)cp, in.get<uint32_t>(),
                          flag.get<int>(), st);
+        if (fsb) {  // binarize into tiles (pack_nhwc then convert), then back to plain for the GEMM
+          launch_convert_act(H, H, batch, c, 0, 0, 0, in.get<uint64_t>(), 1, kBh, kBw, in_t.get<uint64_t>(), st);
+          launch_convert_act(H, H, batch, c, 1, kBh, kBw, in_t.get<uint64_t>(), 0, 0, 0, in.get<uint64_t>(), st);
+        }
+      } else if (fsb) {
+        launch_convert_act(H, H, batch, c, 1, kBh, kBw, in_t.get<uint64_t>(), 0, 0, 0, in.get<uint64_t>(), st);
       }
       used = launch_bgemm(s, in.get<uint64_t>(), filt.get<uint64_t>(), e, st, EngineHint::Auto, &tcf);
+      if (fsb && bin)
+        launch_convert_act(P, P, batch, o, 0, 0, 0, out_b.get<uint64_t>(), 1, kBh, kBw, out_t.get<uint64_t>(), st);
     };
     BT_CUDA(cudaStreamSynchronize(st));
     time_reps(reps, warmup, st, step, median_ns, min_ns);
@@ -317,6 +365,25 @@ int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, siz
     if (engine && engine_len) std::snprintf(engine, engine_len, "%s", used);
     cudaStreamDestroy(st);
   });
+}
+
+int btnn_cuda_bench_bmm(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
+                        size_t engine_len, const btnn_bench_readback* rb) {
+  return bench_bmm_impl(n, bin, 0, reps, warmup, median_ns, min_ns, engine, engine_len, rb);
+}
+int btnn_cuda_bench_bmm_fsb(size_t n, int bin, int reps, int warmup, double* median_ns, double* min_ns, char* engine,
+                            size_t engine_len, const btnn_bench_readback* rb) {
+  return bench_bmm_impl(n, bin, 1, reps, warmup, median_ns, min_ns, engine, engine_len, rb);
+}
+int btnn_cuda_bench_bconv(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps, int warmup,
+                          double* median_ns, double* min_ns, char* engine, size_t engine_len,
+                          const btnn_bench_readback* rb) {
+  return bench_bconv_impl(input_hw, batch, c, o, k, bin, 0, reps, warmup, median_ns, min_ns, engine, engine_len, rb);
+}
+int btnn_cuda_bench_bconv_fsb(size_t input_hw, size_t batch, size_t c, size_t o, size_t k, int bin, int reps,
+                              int warmup, double* median_ns, double* min_ns, char* engine, size_t engine_len,
+                              const btnn_bench_readback* rb) {
+  return bench_bconv_impl(input_hw, batch, c, o, k, bin, 1, reps, warmup, median_ns, min_ns, engine, engine_len, rb);
 }
 
 }  // extern "C"

@@ -464,17 +464,32 @@ void launch_pack_nhwc(const float* x, int N, int H, int W, int C, int n_pad, int
   BT_CUDA(cudaGetLastError());
 }
 
+// Layout conversions. Word path: when source and destination run along the same fast index
+// (RowPacked / fsb_row: columns; ColPacked / fsb_col: rows) and every fsb tile width is a
+// multiple of 64, each destination word is one aligned source word (pad bits masked) — one
+// load per word. Otherwise bit by bit.
 __global__ void convert_matrix_kernel(size_t rows, size_t cols, int sl, size_t sbh, size_t sbw,
                                       const uint64_t* __restrict__ src, int dl, size_t dbh, size_t dbw,
-                                      uint64_t* dst, size_t dst_words) {
+                                      uint64_t* dst, size_t dst_words, int word_path) {
+  const bool row_major = dl == BTNN_ROW_PACKED || dl == BTNN_FSB_ROW;
   for (size_t wi = (size_t)blockIdx.x * blockDim.x + threadIdx.x; wi < dst_words;
        wi += (size_t)gridDim.x * blockDim.x) {
     uint64_t word = 0;
-    for (int b = 0; b < 64; ++b) {
+    if (word_path) {
       size_t r, c;
-      if (mat_inv(rows, cols, dl, dbh, dbw, wi * 64 + b, &r, &c) &&
-          bit_get(src, mat_bit(rows, cols, sl, sbh, sbw, r, c)))
-        word |= 1ull << b;
+      mat_inv(rows, cols, dl, dbh, dbw, wi * 64, &r, &c);  // first bit of the word (fast index % 64 == 0)
+      const size_t fast = row_major ? c : r, nfast = row_major ? cols : rows;
+      if ((row_major ? r < rows : c < cols) && fast < nfast) {
+        word = __ldg(src + mat_bit(rows, cols, sl, sbh, sbw, r, c) / 64);
+        if (nfast - fast < 64) word &= (1ull << (nfast - fast)) - 1ull;
+      }
+    } else {
+      for (int b = 0; b < 64; ++b) {
+        size_t r, c;
+        if (mat_inv(rows, cols, dl, dbh, dbw, wi * 64 + b, &r, &c) &&
+            bit_get(src, mat_bit(rows, cols, sl, sbh, sbw, r, c)))
+          word |= 1ull << b;
+      }
     }
     dst[wi] = word;
   }
@@ -483,26 +498,38 @@ void launch_convert_matrix(size_t rows, size_t cols, int sl, size_t sbh, size_t 
                            size_t dbh, size_t dbw, uint64_t* dst, cudaStream_t st) {
   const size_t words = mat_words(rows, cols, dl, dbh, dbw);
   if (!words) return;
+  auto rowish = [](int l) { return l == BTNN_ROW_PACKED || l == BTNN_FSB_ROW; };
+  auto w64 = [](int l, size_t bw) { return (l != BTNN_FSB_ROW && l != BTNN_FSB_COL) || bw % 64 == 0; };
+  const int word_path = rowish(sl) == rowish(dl) && w64(sl, sbw) && w64(dl, dbw);
   const size_t blocks = (words + 255) / 256;
   convert_matrix_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(
-      rows, cols, sl, sbh, sbw, src, dl, dbh, dbw, dst, words);
+      rows, cols, sl, sbh, sbw, src, dl, dbh, dbw, dst, words, word_path);
   BT_CUDA(cudaGetLastError());
 }
 
 __global__ void convert_act_kernel(size_t h, size_t w, size_t n, size_t c, int st_, size_t sbh, size_t sbw,
                                    const uint64_t* __restrict__ src, int dt, size_t dbh, size_t dbw, uint64_t* dst,
-                                   size_t dst_words) {
+                                   size_t dst_words, int word_path) {
   const size_t dplane = act_npad(n, dt, dbh) * act_cpad(c, dt, dbw) / 64;
   for (size_t wi = (size_t)blockIdx.x * blockDim.x + threadIdx.x; wi < dst_words;
        wi += (size_t)gridDim.x * blockDim.x) {
     const size_t site = wi / dplane, inw = wi % dplane;
     const size_t hh = site / w, ww = site % w;
     uint64_t word = 0;
-    for (int b = 0; b < 64; ++b) {
+    if (word_path) {  // plain and tiled planes both run along channels
       size_t nn, cc;
-      if (act_plane_inv(n, c, dt, dbh, dbw, inw * 64 + b, &nn, &cc) &&
-          bit_get(src, act_bit(w, n, c, st_, sbh, sbw, hh, ww, nn, cc)))
-        word |= 1ull << b;
+      act_plane_inv(n, c, dt, dbh, dbw, inw * 64, &nn, &cc);
+      if (nn < n && cc < c) {
+        word = __ldg(src + act_bit(w, n, c, st_, sbh, sbw, hh, ww, nn, cc) / 64);
+        if (c - cc < 64) word &= (1ull << (c - cc)) - 1ull;
+      }
+    } else {
+      for (int b = 0; b < 64; ++b) {
+        size_t nn, cc;
+        if (act_plane_inv(n, c, dt, dbh, dbw, inw * 64 + b, &nn, &cc) &&
+            bit_get(src, act_bit(w, n, c, st_, sbh, sbw, hh, ww, nn, cc)))
+          word |= 1ull << b;
+      }
     }
     dst[wi] = word;
   }
@@ -511,9 +538,10 @@ void launch_convert_act(size_t h, size_t w, size_t n, size_t c, int st_, size_t 
                         const uint64_t* src, int dt, size_t dbh, size_t dbw, uint64_t* dst, cudaStream_t st) {
   const size_t words = act_words(h, w, n, c, dt, dbh, dbw);
   if (!words) return;
+  const int word_path = (!st_ || sbw % 64 == 0) && (!dt || dbw % 64 == 0);
   const size_t blocks = (words + 255) / 256;
   convert_act_kernel<<<(unsigned)(blocks < 148 * 16 ? blocks : 148 * 16), 256, 0, st>>>(
-      h, w, n, c, st_, sbh, sbw, src, dt, dbh, dbw, dst, words);
+      h, w, n, c, st_, sbh, sbw, src, dt, dbh, dbw, dst, words, word_path);
   BT_CUDA(cudaGetLastError());
 }
 

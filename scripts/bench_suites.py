@@ -12,6 +12,10 @@ throughput_unit,precheck), with the B200 path timed through the C ABI:
   2 P Q N C O K^2 / t (bench.hpp:290-292).
 * model: images/s of the device plan over --batches (graph replay, inputs resident).
 
+Every bmm / bconv size also gets an `fsb` row (bench.hpp:140-156, 230-245): the call's
+operands are the 8 x 128-tile (FSB / tiled) layouts, converted on the device inside each timed
+call (btnn_cuda_bench_bmm_fsb / btnn_cuda_bench_bconv_fsb).
+
 `precheck` follows bench.hpp:164-176 / 248-256: after timing, the device operands and the
 result of the timed call are read back and 256 sampled entries are recomputed on the host
 from the packed words (the +-1 dot n - 2*popc(a ^ b), bit_buffer.hpp:94-113; for BConv the
@@ -38,8 +42,8 @@ HDR = ("suite,kernel,variant,layout,shape,threads,reps,warmup,median_ns,mean_ns,
        "throughput_unit,precheck")
 
 
-def row(suite, kernel, variant, shape, reps, warmup, med, mn, thr, unit, ok):
-    return (f"{suite},{kernel},{variant},plain,{shape},0,{reps},{warmup},{med:.1f},{med:.1f},{mn:.1f},"
+def row(suite, kernel, variant, shape, reps, warmup, med, mn, thr, unit, ok, layout="plain"):
+    return (f"{suite},{kernel},{variant},{layout},{shape},0,{reps},{warmup},{med:.1f},{med:.1f},{mn:.1f},"
             f"{thr:.3f},{unit},{'ok' if ok else 'FAIL'}")
 
 
@@ -75,12 +79,12 @@ def bmm_rows(bin_, reps, warmup, nmin, nmax):
         res = np.zeros(n * kw, np.uint64) if bin_ else np.zeros(n * n, np.int32)
         rb = capi.BenchReadback(a.ctypes.data_as(C.POINTER(C.c_uint64)), b.ctypes.data_as(C.POINTER(C.c_uint64)),
                                 res.ctypes.data_as(C.c_void_p), None)
-        capi.check(lib.btnn_cuda_bench_bmm(n, int(bin_), reps, warmup, C.byref(med), C.byref(mn), eng, 16,
-                                           C.byref(rb)))
-        ops = 2.0 * n ** 3
-        out.append(row("bmm-bin" if bin_ else "bmm", "bmm_pm1_bin" if bin_ else "bmm_pm1", eng.value.decode(),
-                       f"{n}x{n}x{n}", reps, warmup, med.value, mn.value, ops / (med.value * 1e-9), "bitops/s",
-                       bmm_precheck(n, bin_, a, b, res, rng)))
+        for layout, fn in (("plain", lib.btnn_cuda_bench_bmm), ("fsb", lib.btnn_cuda_bench_bmm_fsb)):
+            capi.check(fn(n, int(bin_), reps, warmup, C.byref(med), C.byref(mn), eng, 16, C.byref(rb)))
+            ops = 2.0 * n ** 3
+            out.append(row("bmm-bin" if bin_ else "bmm", "bmm_pm1_bin" if bin_ else "bmm_pm1", eng.value.decode(),
+                           f"{n}x{n}x{n}", reps, warmup, med.value, mn.value, ops / (med.value * 1e-9), "bitops/s",
+                           bmm_precheck(n, bin_, a, b, res, rng), layout))
         n *= 2
     return out
 
@@ -127,12 +131,13 @@ def bconv_rows(bin_, reps, warmup, cmin, cmax, hw=64, batch=16, k=3):
         res = np.zeros(hw * hw * npad * cw, np.uint64) if bin_ else np.zeros(hw * hw * batch * c, np.int32)
         rb = capi.BenchReadback(act.ctypes.data_as(C.POINTER(C.c_uint64)), filt.ctypes.data_as(C.POINTER(C.c_uint64)),
                                 res.ctypes.data_as(C.c_void_p), None)
-        capi.check(lib.btnn_cuda_bench_bconv(hw, batch, c, c, k, int(bin_), reps, warmup, C.byref(med), C.byref(mn),
-                                             eng, 16, C.byref(rb)))
-        ops = 2.0 * hw * hw * batch * c * c * k * k  # border taps counted as full (bench.hpp:290-292)
-        out.append(row("bconv-bin" if bin_ else "bconv", "bconv_fused" if bin_ else "bconv_pm1", eng.value.decode(),
-                       f"{hw}x{hw}x{batch}x{c}->{c}k{k}", reps, warmup, med.value, mn.value,
-                       ops / (med.value * 1e-9), "bitops/s", bconv_precheck(hw, batch, c, c, k, bin_, act, filt, res, rng)))
+        for layout, fn in (("plain", lib.btnn_cuda_bench_bconv), ("fsb", lib.btnn_cuda_bench_bconv_fsb)):
+            capi.check(fn(hw, batch, c, c, k, int(bin_), reps, warmup, C.byref(med), C.byref(mn), eng, 16, C.byref(rb)))
+            ops = 2.0 * hw * hw * batch * c * c * k * k  # border taps counted as full (bench.hpp:290-292)
+            out.append(row("bconv-bin" if bin_ else "bconv", "bconv_fused" if bin_ else "bconv_pm1",
+                           eng.value.decode(), f"{hw}x{hw}x{batch}x{c}->{c}k{k}", reps, warmup, med.value, mn.value,
+                           ops / (med.value * 1e-9), "bitops/s",
+                           bconv_precheck(hw, batch, c, c, k, bin_, act, filt, res, rng), layout))
         c *= 2
     return out
 

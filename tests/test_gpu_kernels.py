@@ -161,13 +161,25 @@ def test_format_stage_vs_harness_packers():
     for lay in range(4):
         assert np.array_equal(B.pack_matrix(v, 17, 300, lay), Wt.pack_matrix(v, 17, 300, lay)), lay
     A = Wt.pack_matrix(v, 17, 300, capi.ROW_PACKED)
-    for geo in ((8, 128), (4, 64), (2, 256), (16, 128)):  # test_bitcore.cpp:168-183 round trips
+    # test_bitcore.cpp:168-183 round trips; widths 32 / 96 take the bit-by-bit conversion
+    # path, multiples of 64 the whole-word one
+    for geo in ((8, 128), (4, 64), (2, 256), (16, 128), (4, 32), (2, 96)):
         f = B.to_fsb(md(17, 300, capi.ROW_PACKED), A, *geo)
         assert np.array_equal(f, Wt.pack_matrix(v, 17, 300, capi.FSB_ROW, *geo))
         assert np.array_equal(B.from_fsb(md(17, 300, capi.FSB_ROW, *geo), f), A)
     ad = capi.ActDesc(5, 7, 3, 130, 0, 8, 128)
     aw = Wt.pack_nhwc(x)
     assert np.array_equal(B.convert_activations(ad, aw, True), Wt.pack_nhwc(x, True))
+    for geo in ((8, 128), (4, 64), (2, 32)):  # tiled -> plain and back, word and bit paths
+        t = B.convert_activations(ad, aw, True, *geo)
+        assert np.array_equal(t, Wt.pack_nhwc(x, True, *geo)), geo
+        assert np.array_equal(B.convert_activations(capi.ActDesc(5, 7, 3, 130, 1, *geo), t, False), aw), geo
+    # column layouts: ColPacked <-> fsb_col
+    Bc = Wt.pack_matrix(v, 17, 300, capi.COL_PACKED)
+    for geo in ((8, 128), (2, 64), (4, 32)):
+        f = B.to_fsb(md(17, 300, capi.COL_PACKED), Bc, *geo)
+        assert np.array_equal(f, Wt.pack_matrix(v, 17, 300, capi.FSB_COL, *geo)), geo
+        assert np.array_equal(B.from_fsb(md(17, 300, capi.FSB_COL, *geo), f), Bc), geo
     flat = x.reshape(3, -1)
     assert np.array_equal(B.flatten_to_matrix(ad, aw, capi.ROW_PACKED), Wt.pack_matrix(flat, 3, flat.shape[1], capi.ROW_PACKED))
     bad = x.copy()
