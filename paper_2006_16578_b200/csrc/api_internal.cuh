@@ -62,9 +62,11 @@ struct TcFilter {
 
 // Geometry of one tensor-core launch, chosen per layer shape by measurement (the plan's
 // tuner, plan.cu): spt > 0 runs halo mode with that many output sites per tile, tmem_a = 1
-// the TMEM-A path; {0, 0} is the cost model's choice (kernels_tc.cu tc_geom).
+// the TMEM-A path, groups the bn route's epilogue groups; {0, 0, 0} is the cost model's
+// choice (kernels_tc.cu tc_geom).
 struct TcChoice {
   int spt = 0, tmem_a = 0;
+  int groups = 0;  // bn route: epilogue groups / TMEM accumulators (2 or 3; 0 = automatic)
 };
 // The distinct feasible geometries of (s, e), the cost model's own first; "halo/sptN" or
 // "tmemA" names them.

@@ -650,7 +650,8 @@ int btnn_cuda_plan_layer_choice(btnn_plan* plan, size_t i, char* buf, size_t n, 
     std::string out;
     size_t pick = 0;
     for (size_t k = 0; k < L.cands.size(); ++k)
-      if (L.cands[k].spt == L.choice.spt && L.cands[k].tmem_a == L.choice.tmem_a) pick = k;
+      if (L.cands[k].spt == L.choice.spt && L.cands[k].tmem_a == L.choice.tmem_a && L.cands[k].groups == L.choice.groups)
+        pick = k;
     for (size_t k = 0; k < L.cands.size(); ++k) {
       out += (k ? "," : "") + std::string(k == pick ? "*" : "") + L.cand_names[k];
       if (ms && k < n_ms) ms[k] = L.cand_ms[k];

@@ -68,7 +68,8 @@ def _assert_launch(expect, exclude=()):
         assert part in variant.split("/"), (variant, expect)
     for part in exclude:
         assert part not in variant.split("/"), (variant, exclude)
-    assert units >= 3 * grid, f"{variant}: {units} units on {grid} CTAs — fewer than 3 per CTA"
+    if not variant.startswith("bmm_packed"):  # (one tile per CTA by design: not persistent)
+        assert units >= 3 * grid, f"{variant}: {units} units on {grid} CTAs — fewer than 3 per CTA"
     return variant
 
 
@@ -126,17 +127,19 @@ def test_tc_variant_many_tiles_per_cta(case):
         capi.set_engine(capi.ENGINE_AUTO)
 
 
-def test_bmm_many_tiles_per_cta():
-    """BMM 8192 x 1024 x 1024 (512 output tiles) packed -> int32 and -> thresholded bits."""
+@pytest.mark.parametrize("kk,kind_", [(1024, "bmm_packed"), (2048, "tmemA")])
+def test_bmm_many_tiles_per_cta(kk, kind_):
+    """BMM 8192 x K x 1024 packed -> int32 and -> thresholded bits: K = 1024 runs the one-kernel
+    packed BMM (1024 CTAs), K = 2048 the implicit GEMM with 512 tiles over the persistent CTAs."""
     capi.set_engine(capi.ENGINE_TC)
     try:
         rng = np.random.default_rng(9)
-        m, kk, nn = 8192, 1024, 1024
+        m, nn = 8192, 1024
         A = rng.integers(0, 2**64, m * kk // 64, dtype=np.uint64)
         Bw = rng.integers(0, 2**64, nn * kk // 64, dtype=np.uint64)
         da, db = capi.MatrixDesc(m, kk, capi.ROW_PACKED, 8, 128), capi.MatrixDesc(kk, nn, capi.COL_PACKED, 8, 128)
         got = B.bmm_pm1(da, A, db, Bw).reshape(-1)
-        _assert_launch(("tmemA", "i32"))
+        _assert_launch((kind_, "i32"))
         want = np.zeros(m * nn, np.int32)
         assert oracle().bo_bmm_pm1(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64), capi.BMM_BLOCKED,
                                    ptr(want, C.c_int32)) == 0
@@ -144,7 +147,7 @@ def test_bmm_many_tiles_per_cta():
         tau = rng.standard_normal(nn) * 20
         kind = rng.integers(0, 4, nn).astype(np.uint8)
         bits = B.bmm_pm1_bin(da, A, db, Bw, tau=tau, kind=kind)
-        _assert_launch(("tmemA", "thr"))
+        _assert_launch((kind_, "bin" if kind_ == "bmm_packed" else "thr"))
         wbits = np.zeros_like(bits)
         assert oracle().bo_bmm_pm1_bin(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64),
                                        capi.BMM_BLOCKED, ptr(np.ascontiguousarray(tau), C.c_double),
