@@ -50,3 +50,10 @@ if m[:, 0].any() and not t[1024 + 16 * 32:1024 + 16 * 32 + 1].any():
         r = m[u]
         if r[0]:
             print(u, [int(v - r[0]) for v in r[:9]])
+p = t[2304:2304 + 320].reshape(40, 8)
+if p[:, 0].any():
+    print("producer thread 0 per K-step (i = 10..): issue | cp-wait | expand | st-wait+arrive | ->empty-wait | empty-wait | st (clk)")
+    for k in range(12):
+        r = p[k]
+        if r[0]:
+            print(k + 10, [int(r[j + 1] - r[j]) for j in range(7)])
