@@ -442,6 +442,7 @@ def run_model(a, rank, world, local, dist):
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
+    torch.cuda.profiler.start()  # (ncu --profile-from-start off captures the timed steps only)
     with Clocks(local) as clk:
         if flush is None:
             ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -461,6 +462,7 @@ def run_model(a, rank, world, local, dist):
                 e1.record(stream)
                 torch.cuda.synchronize(dev)
                 ms += e0.elapsed_time(e1)
+    torch.cuda.profiler.stop()
     if dist:
         dist.barrier()
         ms = D.max_over_ranks(ms, dev)

@@ -298,6 +298,10 @@ int btnn_cuda_plan_run(btnn_plan* plan, const float* x, size_t batch, double* lo
  * pointers on that device; stream is a cudaStream_t (NULL = the plan's stream). Async. */
 int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size_t batch,
                               double* d_logits, int32_t* d_labels, void* stream);
+/* After a plan_run_device has completed (the caller synchronized its stream): 1 when that
+ * run's input held a non-finite value — the condition under which run_inference throws
+ * invalid_input (inference.hpp:69-75); the device run's logits are then not the reference's. */
+int btnn_cuda_plan_input_status(btnn_plan* plan, int shard, int* nonfinite);
 /* Per-layer device time of the last plan_run on shard 0, ms (RunOptions::breakdown,
  * inference.hpp:169-174). n_layers entries. */
 int btnn_cuda_plan_layer_ms(btnn_plan* plan, double* ms, size_t n_layers);

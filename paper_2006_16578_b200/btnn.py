@@ -255,6 +255,13 @@ class Plan:
         check(lib().btnn_cuda_plan_run_device(self.h, shard, C.c_void_p(d_x), batch, C.c_void_p(d_logits or None),
                                               C.c_void_p(d_labels or None), C.c_void_p(stream or None)))
 
+    def input_status(self, shard: int = 0) -> bool:
+        """True when the last completed run_device on `shard` saw a non-finite input value
+        (run_inference's invalid_input condition)."""
+        f = C.c_int()
+        check(lib().btnn_cuda_plan_input_status(self.h, shard, C.byref(f)))
+        return bool(f.value)
+
     def set_breakdown(self, on: bool):
         check(lib().btnn_cuda_plan_set_breakdown(self.h, int(on)))
 

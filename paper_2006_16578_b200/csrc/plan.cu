@@ -759,9 +759,24 @@ int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size
     require(batch > 0 && batch <= sh.max_batch, BTNN_INVALID_INPUT, "plan_run_device: batch out of range");
     BT_CUDA(cudaSetDevice(sh.device));
     // stream == NULL: the plan's own stream (caller synchronizes via the device);
-    // otherwise the graph is launched straight onto the caller's stream.
+    // otherwise the graph is launched straight onto the caller's stream. The input check's
+    // non-finite flag is cleared first and read back by btnn_cuda_plan_input_status.
+    cudaStream_t ls = stream ? static_cast<cudaStream_t>(stream) : sh.stream;
+    BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), ls));
     run_shard_device(plan, sh, d_x, batch, d_logits ? d_logits : sh.logits.get<double>(),
                      d_labels ? d_labels : sh.labels.get<int32_t>(), false, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int btnn_cuda_plan_input_status(btnn_plan* plan, int shard, int* nonfinite) {
+  return guard([&] {
+    require(plan && shard >= 0 && (size_t)shard < plan->shards.size() && nonfinite, BTNN_INVALID_INPUT,
+            "plan_input_status: bad arguments");
+    Shard& sh = *plan->shards[shard];
+    BT_CUDA(cudaSetDevice(sh.device));
+    int f = 0;
+    BT_CUDA(cudaMemcpy(&f, sh.flag.get(), sizeof(int), cudaMemcpyDeviceToHost));
+    *nonfinite = f != 0;
   });
 }
 

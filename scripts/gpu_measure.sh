@@ -19,5 +19,5 @@ if [ -z "$NOSUITES" ]; then
   for s in bmm bmm-bin bconv bconv-bin; do timeout 600 python scripts/bench_suites.py --suite $s --csv $O/suite_$s.csv > /dev/null 2>&1; echo "suite $s rc=$?"; done
   timeout 600 python scripts/bench_suites.py --suite model --model resnet18 --batches 8,64,256,512,1024,2048,4096 --csv $O/suite_model_resnet18.csv > /dev/null 2>&1; echo "suite model rc=$?"
 fi
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_resnet18_b512.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-kernels > $O/ncu_l.log 2>&1; echo "ncu-l rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"first_conv_tc_kernel|bgemm_tc_kernel" -c 17 -o $O/resnet18_b512_full python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-kernels > $O/ncu_full.log 2>&1; echo "ncu-full rc=$?"
+timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_resnet18_b512.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-kernels > $O/ncu_l.log 2>&1; echo "ncu-l rc=$?"
+timeout 1200 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"first_conv_tc_kernel|bgemm_tc_kernel" -c 17 -o $O/resnet18_b512_full python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-kernels > $O/ncu_full.log 2>&1; echo "ncu-full rc=$?"

@@ -217,3 +217,24 @@ def test_every_tuner_candidate_bit_exact(prefix, fm, engine):
             assert np.array_equal(lg.view(np.uint64), fm.logits.view(np.uint64)), (i, names[k], plan.engines())
         if names:
             plan.set_layer_choice(i, pick)
+
+
+def test_device_run_reports_nonfinite_input(engine):
+    """plan_run_device cannot throw mid-stream; input_status reports run_inference's
+    invalid_input condition for the last device run (and clears for a finite input)."""
+    import torch
+    m = M.make_model("bad", "8C3-8FC", 8, 8, 3, 3)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 5))
+    plan = B.Plan(m, ws, 4)
+    x = torch.randn((4, 8, 8, 3), dtype=torch.float32, device="cuda")
+    plan.run_device(x.data_ptr(), 4)
+    torch.cuda.synchronize()
+    assert not plan.input_status()
+    x[2, 3, 4, 1] = float("inf")
+    plan.run_device(x.data_ptr(), 4)
+    torch.cuda.synchronize()
+    assert plan.input_status()
+    x[2, 3, 4, 1] = 0.5
+    plan.run_device(x.data_ptr(), 4)
+    torch.cuda.synchronize()
+    assert not plan.input_status()
