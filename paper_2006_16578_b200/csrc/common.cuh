@@ -83,6 +83,25 @@ inline int timing_knob(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
+// Launch with programmatic stream serialization (the kernel calls grid_dep_wait before it
+// touches data of earlier kernels): its prologue (barrier init, TMEM allocation, tables,
+// static weights) overlaps the previous kernel's tail; in a captured graph the dependency
+// becomes a programmatic edge.
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  BT_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 template <class T>
 DevBuf upload(const T* host, size_t count, cudaStream_t st) {
   DevBuf b(count * sizeof(T));

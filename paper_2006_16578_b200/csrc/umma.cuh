@@ -51,6 +51,13 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) __nanosleep(NS);
 }
 
+// Programmatic dependent launch (kernels launched with programmatic stream serialization):
+// launch_dependents lets the next kernel in the stream start its prologue on SMs this grid
+// has freed; wait blocks until every prerequisite grid has completed and its memory is visible
+// — called before the first access to anything an earlier kernel writes or reads.
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // One elected lane of a converged warp (elect.sync).
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
