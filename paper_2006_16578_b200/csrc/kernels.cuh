@@ -92,8 +92,12 @@ void launch_first_conv_tc_weights(const float* w_pm1, int O, int KH, int KW, int
 // Input check per row (n, h) of W*C floats: non-finite flag + largest |x| bit pattern.
 void launch_input_rows(const float* x, size_t rows, int row_len, int* flag, uint32_t* rowmax, cudaStream_t st);
 // rowmax from launch_input_rows; fix_list holds up to N*P*Q window ids.
+// True when the tensor-core first conv can take the tile maxima and the input check itself
+// (rowmax == nullptr, flag in nonfinite): stride 4, one pixel column per builder thread, and
+// the windows cover every input row (so every input value is checked).
+bool first_conv_fused_input(const FirstConvArgs& a);
 void launch_first_conv_tc(const FirstConvArgs& a, const uint32_t* rowmax, const int8_t* wblk, int* fix_count,
-                          int* fix_list, cudaStream_t st);
+                          int* fix_list, cudaStream_t st, int* nonfinite = nullptr);
 bool try_first_conv_tc_standalone(const FirstConvArgs& a, cudaStream_t st);
 
 // Format stage.

@@ -310,12 +310,17 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     first_tc = engine_override() != BTNN_ENGINE_POPC && first_conv_tc_supported(fa);
   }
   if (timed) BT_CUDA(cudaEventRecord(sh.events[0], st));  // layer 0's time includes the input pass
-  if (first_tc)
+  // the first conv's own builders check the input and take the tile maxima where they cover it
+  const bool fused_in = first_tc && first_conv_fused_input(fa);
+  if (fused_in) {
+  } else if (first_tc) {
     launch_input_rows(d_x, batch * plan->in_h, (int)(plan->in_w * plan->in_c), sh.flag.get<int>(),
                       sh.rowmax.get<uint32_t>(), st);
-  else
+    ++launches;
+  } else {
     launch_check_finite(d_x, batch * plan->in_h * plan->in_w * plan->in_c, sh.flag.get<int>(), st);
-  ++launches;
+    ++launches;
+  }
   const size_t np = act_npad(batch, 0, 0);
   int cur = 0;              // act buffer holding the current activations
   int fcur = 0;             // fc buffer holding the current fc activations
@@ -351,8 +356,8 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       a.cwo = (int)(act_cpad(l.out_channels, 0, 0) / 64);
       a.pool = pool;
       if (first_tc) {
-        launch_first_conv_tc(a, sh.rowmax.get<uint32_t>(), L.wblk.get<int8_t>(), L.fix_count.get<int>(),
-                             L.fix_list.get<int>(), st);
+        launch_first_conv_tc(a, fused_in ? nullptr : sh.rowmax.get<uint32_t>(), L.wblk.get<int8_t>(), L.fix_count.get<int>(),
+                             L.fix_list.get<int>(), st, sh.flag.get<int>());
         launches += 2;
         L.engine = pool ? "tc_i8_exact+pool" : "tc_i8_exact";
       } else {

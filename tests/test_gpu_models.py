@@ -238,3 +238,29 @@ def test_device_run_reports_nonfinite_input(engine):
     plan.run_device(x.data_ptr(), 4)
     torch.cuda.synchronize()
     assert not plan.input_status()
+
+
+def test_fused_input_check_of_stride4_first_conv(engine):
+    """The 7x7/4 first conv checks the input itself (no separate input pass): a non-finite
+    value anywhere is still run_inference's invalid_input, through plan_run and through
+    plan_run_device's status, and finite inputs stay bit-exact."""
+    import torch
+    m = M.make_model("s4", "32C7/4-32C3-10FC", 32, 32, 3, 10)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 91))
+    x = np.random.default_rng(92).standard_normal((5, 32, 32, 3), dtype=np.float32)
+    plan = B.Plan(m, ws, 5)
+    lg, lb = plan.run(x)
+    want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+    assert np.array_equal(lg.view(np.uint64), want.view(np.uint64)) and np.array_equal(lb, wl)
+    for pos, val in (((4, 31, 31, 2), np.inf), ((0, 0, 0, 0), np.nan), ((2, 17, 5, 1), -np.inf)):
+        bad = x.copy()
+        bad[pos] = val
+        with pytest.raises(capi.BtnnError) as e:
+            plan.run(bad)
+        assert e.value.code == capi.BTNN_INVALID_INPUT
+        xd = torch.from_numpy(bad).cuda()
+        plan.run_device(xd.data_ptr(), 5)
+        torch.cuda.synchronize()
+        assert plan.input_status()
+    lg2, _ = plan.run(x)
+    assert np.array_equal(lg2.view(np.uint64), want.view(np.uint64))
