@@ -9,8 +9,10 @@ def main(path, out, title):
     hdr = rows[0]
     ik, im, iv, iid = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("ID")
     ks = [(int(r[iid]), r[ik], float(r[iv].replace(",", ""))) for r in rows[1:] if r[im] == "gpu__time_duration.sum"]
-    # the step: from the first input_rows_kernel to the next argmax_kernel (inclusive)
+    # the step: from the first input pass (or first conv) to the next argmax_kernel (inclusive)
     starts = [i for i, k in enumerate(ks) if "input_rows" in k[1] or "check_finite" in k[1]]
+    if not starts:  # the first conv checks its input itself (fused input pass): it opens the step
+        starts = [i for i, k in enumerate(ks) if "first_conv" in k[1]]
     s0 = starts[0]
     e0 = next(i for i in range(s0, len(ks)) if "argmax" in ks[i][1])
     step = ks[s0:e0 + 1]
