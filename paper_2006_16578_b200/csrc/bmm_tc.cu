@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "api_internal.cuh"
+#include "bnmath.cuh"
 #include "kernels.cuh"
 #include "pm1.cuh"
 #include "umma.cuh"
@@ -41,6 +42,8 @@ struct BmmTcArgs {
   int mode;                // EPI_I32 (raw or pm1) or EPI_BITS
   int raw;                 // EPI_I32: (K - v) / 2
   int32_t* out;            // M x N int32
+  double* rout;            // EPI_F64: M x N f64 bn(v) (the last layer's logits)
+  const double *bn_mean, *bn_s, *bn_rcp, *bn_gamma, *bn_beta;  // EPI_F64
   uint32_t* out_bits;      // RowPacked M x (cwo * 64) bits, as 32-bit words
   int cwo32;               // output words (32-bit) per row
   const long long* thr_lo;  // EPI_BITS: per column lo / hi (nullptr: v >= 0)
@@ -84,6 +87,7 @@ __global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid
   __shared__ uint64_t mma_done;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int2 thr[bmmtc::kBN];  // EPI_BITS: per column (lo, width) of the range test
+  __shared__ double bnp[5][bmmtc::kBN];  // EPI_F64: per column mean, s, rcp, gamma, beta
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q = warp & 3, part = warp >> 2;  // TMEM lane quarter, and which quarter of the work
   const int m0 = blockIdx.y * bmmtc::kBM, n0 = blockIdx.x * bmmtc::kBN;
@@ -131,6 +135,14 @@ __global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid
       w = lc > hc ? 0u : (uint32_t)(hc - lc);
     }
     thr[tid] = make_int2(lo32, (int)w);
+  }
+  if (p.mode == EPI_F64 && tid < bmmtc::kBN) {
+    const int n = min(n0 + tid, p.N - 1);
+    bnp[0][tid] = p.bn_mean[n];
+    bnp[1][tid] = p.bn_s[n];
+    bnp[2][tid] = p.bn_rcp ? p.bn_rcp[n] : 0.0;
+    bnp[3][tid] = p.bn_gamma[n];
+    bnp[4][tid] = p.bn_beta[n];
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   BMM_STAMP(1)
@@ -232,6 +244,36 @@ __global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid
         if (ncol < 16) word &= (1u << ncol) - 1u;
         reinterpret_cast<uint16_t*>(p.out_bits)[(size_t)row * p.cwo32 * 2 + (n0 + c0) / 16] = (uint16_t)word;
       }
+    } else if (p.mode == EPI_F64) {
+      // bn (bnmath.cuh: the reference's (v - mean) / s * gamma + beta, exactly) -> f64 rows
+      // through shared memory (B's expanded tile is dead): rows of 64 doubles at a 528-byte
+      // pitch, then each warp instruction writes one full 512-byte output row segment
+      constexpr int kPitch = 66;  // doubles per staged row
+      double* st = reinterpret_cast<double*>(smem);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        double2 y;
+        y.x = bn_apply((double)(int)acc[j], bnp[0][c0 + j], bnp[1][c0 + j], bnp[2][c0 + j], bnp[3][c0 + j],
+                       bnp[4][c0 + j]);
+        y.y = bn_apply((double)(int)acc[j + 1], bnp[0][c0 + j + 1], bnp[1][c0 + j + 1], bnp[2][c0 + j + 1],
+                       bnp[3][c0 + j + 1], bnp[4][c0 + j + 1]);
+        *reinterpret_cast<double2*>(st + r * kPitch + c0 + j) = y;
+      }
+      __syncthreads();
+      const bool vec = (p.N & 1) == 0 && n0 + bmmtc::kBN <= p.N;
+      for (int rr = warp; rr < bmmtc::kBM; rr += bmmtc::kThreads / 32) {
+        const int orow = m0 + rr;
+        if (orow >= p.M) break;
+        const int cc = lane * 2;
+        double* dst = p.rout + (size_t)orow * p.N + n0 + cc;
+        const double2 v = *reinterpret_cast<const double2*>(st + rr * kPitch + cc);
+        if (vec) {
+          *reinterpret_cast<double2*>(dst) = v;
+        } else {
+          if (n0 + cc < p.N) dst[0] = v.x;
+          if (n0 + cc + 1 < p.N) dst[1] = v.y;
+        }
+      }
     } else {
       // through shared memory (B's expanded tile is dead once the MMAs completed): rows of 64
       // int32 at a 272-byte pitch (16-byte stores of consecutive rows hit different banks),
@@ -292,6 +334,12 @@ void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, co
   p.cwo32 = (N + 127) / 128 * 4;
   p.thr_lo = e.thr_lo;
   p.thr_hi = e.thr_hi;
+  p.rout = e.rout;
+  p.bn_mean = e.bn_mean;
+  p.bn_s = e.bn_s;
+  p.bn_rcp = e.bn_rcp;
+  p.bn_gamma = e.bn_gamma;
+  p.bn_beta = e.bn_beta;
   // One CTA per SM: each allocates all 512 TMEM columns, so a second co-resident CTA would
   // block in tcgen05.alloc until the first exits — request enough smem that two never fit.
   const int smem = std::max(bmmtc::kBN * p.Kp + (bmmtc::kBM + bmmtc::kBN) * p.Kp / 8, 120 * 1024);
@@ -307,7 +355,8 @@ void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, co
   const dim3 grid((unsigned)((N + bmmtc::kBN - 1) / bmmtc::kBN), (unsigned)((M + bmmtc::kBM - 1) / bmmtc::kBM));
   bmm_tc_kernel<<<grid, bmmtc::kThreads, smem, st>>>(p);
   BT_CUDA(cudaGetLastError());
-  note_tc_launch(e.mode == EPI_BITS ? "bmm_packed/bin" : "bmm_packed/i32", (int)(grid.x * grid.y), (int)(grid.x * grid.y));
+  note_tc_launch(e.mode == EPI_BITS ? "bmm_packed/bin" : e.mode == EPI_F64 ? "bmm_packed/bn" : "bmm_packed/i32",
+                 (int)(grid.x * grid.y), (int)(grid.x * grid.y));
 }
 
 }  // namespace btnn_gpu

@@ -39,6 +39,15 @@ const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t
   require(e.rout_half == nullptr || (tc_ok && h != EngineHint::Popc), BTNN_CUDA_ERROR,
           "halved tap output needs the tensor-core engine");
   if (tc_ok && h != EngineHint::Popc) {
+    // fully-connected layers whose inner dimension fits it: the one-kernel packed BMM
+    // (bmm_tc.cu) from the RowPacked activations and the ColPacked weights — threshold bits or
+    // the last layer's bn logits
+    const bool fc = s.P == 1 && s.Q == 1 && s.KH == 1 && s.KW == 1 && s.pad == 0 && !e.rin && !e.rout_half && !e.pool;
+    if (fc && bmm_tc_supported(s.N, s.O, s.C) &&
+        ((e.mode == EPI_BITS && !e.bn_mean && e.out_bits) || (e.mode == EPI_F64 && e.bn_mean && e.rout))) {
+      launch_bmm_tc(s.N, s.O, s.C, act, filt, e, st);
+      return "tc_i8_bmm";
+    }
     return launch_bgemm_tc(s, act, *tc, e, st, ch) ? "tc_i8_splitk" : "tc_i8";
   }
   launch_bgemm_popc(s, act, filt, e, st);
