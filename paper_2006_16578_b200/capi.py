@@ -102,6 +102,7 @@ _PROTOS = {
     "btnn_cuda_device_count": (C.c_int, [P(C.c_int)]),
     "btnn_cuda_set_device": (C.c_int, [C.c_int]),
     "btnn_cuda_set_engine": (C.c_int, [C.c_int]),
+    "btnn_cuda_set_bmm_kernel": (C.c_int, [C.c_int]),
     "btnn_cuda_matrix_words": (sz, [P(MatrixDesc)]),
     "btnn_cuda_act_words": (sz, [P(ActDesc)]),
     "btnn_cuda_filter_words": (sz, [P(FilterDesc)]),
@@ -184,3 +185,11 @@ def last_tc_launch():
 def set_engine(engine: int) -> None:
     """btnn_cuda_set_engine: 0 auto, 1 LOP3+POPC, 2 tcgen05 tensor cores."""
     check(lib().btnn_cuda_set_engine(engine))
+
+
+BMM_AUTO, BMM_WHOLE_K, BMM_PIPELINED = range(3)
+
+
+def set_bmm_kernel(which: int) -> None:
+    """btnn_cuda_set_bmm_kernel: 0 auto, 1 whole-K on-chip kernel (K <= 1536), 2 K-pipelined."""
+    check(lib().btnn_cuda_set_bmm_kernel(which))

@@ -92,5 +92,14 @@ void note_tc_launch(const char* variant, int units, int grid);
 // ColPacked b (N x K), K rounded up to 128 bits <= 1536; EPI_I32 (raw / pm1) or EPI_BITS.
 bool bmm_tc_supported(int M, int N, int K);
 void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st);
+// K-pipelined packed BMM for any inner dimension (bmm_tc.cu, bmm_pipe_kernel): same operands
+// and epilogues as launch_bmm_tc.
+void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st);
+// Either of the two per btnn_cuda_set_bmm_kernel (auto: whole-K when it fits); returns the
+// engine name ("tc_i8_bmm" / "tc_i8_bmm_pipe").
+const char* launch_bmm_packed(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e,
+                              cudaStream_t st);
+// Fully-connected plan layers: a packed kernel when it suits the shape, else nullptr.
+const char* launch_bmm_fc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st);
 
 }  // namespace btnn_gpu

@@ -222,18 +222,16 @@ static int bench_bmm_impl(size_t n, int bin, int fsb, int reps, int warmup, doub
         launch_convert_matrix(n, n, BTNN_ROW_PACKED, 0, 0, out_b.get<uint64_t>(), BTNN_FSB_ROW, kBh, kBw, of.get<uint64_t>(), st);
     };
     TcFilter tcf;
-    const bool packed = engine_override() != BTNN_ENGINE_POPC && bmm_tc_supported((int)n, (int)n, (int)n);
+    const bool packed = engine_override() != BTNN_ENGINE_POPC;
     const bool tc = !packed && engine_override() != BTNN_ENGINE_POPC && tc_supported(s, e);
     if (tc) tc_prepare_filter(s, b.get<uint64_t>(), tcf, st);
     const char* used = "popc";
     // the whole bmm_pm1 / bmm_pm1_bin call from packed operands: one kernel that expands both
-    // operands on chip (bmm_tc.cu) when K fits it; else B's tensor-core operand is re-expanded
-    // every call and the implicit GEMM runs
+    // operands on chip (bmm_tc.cu, whole-K or K-pipelined)
     auto step = [&] {
       to_plain();
       if (packed) {
-        launch_bmm_tc((int)n, (int)n, (int)n, opa, opb, e, st);
-        used = "tc_i8";
+        used = launch_bmm_packed((int)n, (int)n, (int)n, opa, opb, e, st);
       } else {
         if (tc) tc_prepare_filter(s, opb, tcf, st);
         used = launch_bgemm(s, opa, opb, e, st, EngineHint::Auto, &tcf);
@@ -247,7 +245,7 @@ static int bench_bmm_impl(size_t n, int bin, int fsb, int reps, int warmup, doub
     // the GEMM alone with B prepared, and the whole call.
     if (rb && rb->kernel_ns)
       *rb->kernel_ns = time_graph(reps, warmup, st, [&] {
-        if (packed) launch_bmm_tc((int)n, (int)n, (int)n, opa, opb, e, st);
+        if (packed) launch_bmm_packed((int)n, (int)n, (int)n, opa, opb, e, st);
         else launch_bgemm(s, opa, opb, e, st, EngineHint::Auto, &tcf);
       });
     if (rb && rb->stream_ns) *rb->stream_ns = time_stream(reps, warmup, st, step);

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 
 #include "api_internal.cuh"
@@ -359,7 +360,375 @@ void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, co
                  (int)(grid.x * grid.y), (int)(grid.x * grid.y));
 }
 
+// ---------------------------------------------------------------------------------------------
+// K-pipelined variant for any inner dimension (bmm_pipe_kernel<BN>): 128 x BN output tiles,
+// 8 warps, up to two CTAs per SM. Per K-step of 128 bits:
+//   * one 16-byte cp.async per A row / B column stages the packed bits kPD steps ahead;
+//   * all warps expand step s — A row by row to +-1 bytes into a TMEM ring slot (tcgen05.st,
+//     32 columns), B to {0,1} bytes (bit set -> 1, bits past K -> 0; two instructions per
+//     output word instead of three) into a shared-memory ring slot (canonical K-major, 8 core
+//     columns of 16 B per 8-column group) — while the MMAs of step s - 1 run; the A threads
+//     also count their row's set bits below K (pa);
+//   * thread 0 issues the step's four M128 x BN x K32 kind::i8 MMAs (A from TMEM) and commits
+//     them to the slot's mbarrier, which the expansion of step s + kR waits for.
+// The accumulator holds d = sum(a * b01) over K; the +-1 dot is v = sum(a) - 2 d =
+// K - 2 pa - 2 d, read once at the end by the same epilogues as bmm_tc_kernel (int32 /
+// thresholded bits / exact bn logits).
+namespace bmmp {
+constexpr int kR = 4;          // ring depth: expanded B slots (smem) and A slots (TMEM)
+constexpr int kPD = 4;         // packed-bit prefetch distance in K-steps
+constexpr int kPS = kPD + 1;   // packed staging slots
+template <int BN>
+struct Smem {
+  // 8 warps (16 for BN = 256, one CTA per SM); TMEM: BN accumulator + kR x 32 A columns
+  static constexpr int kThreads = BN == 256 ? 512 : 256;
+  static constexpr int kHG = kThreads / 128;  // warps per TMEM lane quarter
+  static constexpr int kTmemCols = BN == 256 ? 512 : 256;
+  static constexpr int kStage = (128 + BN) * 16;  // packed bits of one K-step
+  static constexpr int kBSlot = BN * 128;         // expanded B of one K-step
+  static constexpr int kOffStage = kR * kBSlot;
+  static constexpr int kMain = kOffStage + kPS * kStage;
+  static constexpr int kEpi = 128 * 68 * 8;       // epilogue staging: 128 rows x 64 columns
+  // >= 80 KB: at most two CTAs per SM, so their TMEM allocations always fit
+  static constexpr int kBytes = (kMain > kEpi ? kMain : kEpi) > 80 * 1024 ? (kMain > kEpi ? kMain : kEpi) : 80 * 1024;
+};
+}  // namespace bmmp
+
+template <int BN>
+__global__ void __launch_bounds__(bmmp::Smem<BN>::kThreads, BN == 256 ? 1 : 2)
+    bmm_pipe_kernel(const __grid_constant__ BmmTcArgs p) {
+  using namespace umma;
+  using L = bmmp::Smem<BN>;
+  constexpr int kThreads = L::kThreads, kHG = L::kHG, kWA = 4 / kHG;  // A words per thread
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t mma_done[bmmp::kR];
+  __shared__ uint64_t acc_done;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int2 thr[BN];
+  __shared__ double bnp[5][BN];
+  __shared__ int pa_sh[kHG][128];  // per A row: set bits below K, per word share
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, h = warp >> 2;  // TMEM lane quarter, share of the work
+  int pa = 0;
+  const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
+  const int KS = p.Kp / 128;  // K-steps = 16-byte chunks per packed row
+  uint8_t* bring = smem;
+  uint8_t* stage = smem + L::kOffStage;
+  const uint8_t* ga = reinterpret_cast<const uint8_t*>(p.a);
+  const uint8_t* gb = reinterpret_cast<const uint8_t*>(p.b);
+  // packed bits of K-step s -> staging slot s % kPS (threads 0-127: A rows, 128-: B columns);
+  // every thread commits a group per call, so group counts stay uniform
+  auto issue = [&](int s) {
+    if (s < KS) {
+      uint8_t* dst = stage + (size_t)(s % bmmp::kPS) * L::kStage;
+      if (tid < 128) {
+        const int row = m0 + tid;
+        const bool ok = row < p.M;
+        cp_async16(smem_u32(dst + tid * 16), ga + ((size_t)(ok ? row : 0) * KS + s) * 16, ok ? 16 : 0);
+      } else if (tid < 128 + BN) {
+        const int col = n0 + tid - 128;
+        const bool ok = col < p.N;
+        cp_async16(smem_u32(dst + tid * 16), gb + ((size_t)(ok ? col : 0) * KS + s) * 16, ok ? 16 : 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < bmmp::kPD; ++s) issue(s);
+  if (tid == 0) {
+    for (int r = 0; r < bmmp::kR; ++r) mbar_init(&mma_done[r], 1);
+    mbar_init(&acc_done, 1);
+    fence_mbar_init();
+  }
+  if (p.mode == EPI_BITS && tid < BN) {  // (v - lo) <= width, as in bmm_tc_kernel
+    int lo32 = 0;
+    uint32_t w = 1u << 30;
+    const int n = min(n0 + tid, p.N - 1);
+    if (p.thr_lo) {
+      const long long l = p.thr_lo[n], hh = p.thr_hi[n];
+      const long long lc = l < -(1ll << 30) ? -(1ll << 30) : l, hc = hh > (1ll << 30) ? (1ll << 30) : hh;
+      lo32 = lc > hc ? (1 << 30) + 1 : (int)lc;
+      w = lc > hc ? 0u : (uint32_t)(hc - lc);
+    }
+    thr[tid] = make_int2(lo32, (int)w);
+  }
+  if (p.mode == EPI_F64 && tid < BN) {
+    const int n = min(n0 + tid, p.N - 1);
+    bnp[0][tid] = p.bn_mean[n];
+    bnp[1][tid] = p.bn_s[n];
+    bnp[2][tid] = p.bn_rcp ? p.bn_rcp[n] : 0.0;
+    bnp[3][tid] = p.bn_gamma[n];
+    bnp[4][tid] = p.bn_beta[n];
+  }
+  if (warp == 0) tmem_alloc(&tmem_base_sh, L::kTmemCols);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  const uint32_t idesc = idesc_i8(128, BN);
+  for (int s = 0; s < KS; ++s) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(bmmp::kPD - 1) : "memory");
+    __syncthreads();  // step s staged by every thread; step s - 1's staging slot fully read
+    issue(s + bmmp::kPD);
+    const int r = s % bmmp::kR;
+    if (s >= bmmp::kR) mbar_wait(&mma_done[r], (uint32_t)((s / bmmp::kR - 1) & 1));  // ring slot free
+    const uint8_t* stg = stage + (size_t)(s % bmmp::kPS) * L::kStage;
+    {  // A: row q*32 + lane, 32-bit words kWA*h .. of the step -> 8 TMEM columns each
+      const uint32_t col = (uint32_t)(BN + r * 32 + 8 * kWA * h);
+      const int rem = p.K - 32 * (4 * s + kWA * h);  // valid bits of the first word
+      auto valid = [](int r_) { return r_ >= 32 ? ~0u : r_ > 0 ? (1u << r_) - 1u : 0u; };
+      if constexpr (kWA == 2) {
+        const uint2 bits = *reinterpret_cast<const uint2*>(stg + (q * 32 + lane) * 16 + 8 * h);
+        uint32_t v0[8], v1[8];
+        expand_word(bits.x, v0);
+        expand_word(bits.y, v1);
+        tmem_st8(taddr(tbase, q * 32, col), v0);
+        tmem_st8(taddr(tbase, q * 32, col + 8), v1);
+        pa += __popc(bits.x & valid(rem)) + __popc(bits.y & valid(rem - 32));
+      } else {
+        const uint32_t bits = *reinterpret_cast<const uint32_t*>(stg + (q * 32 + lane) * 16 + 4 * h);
+        uint32_t v0[8];
+        expand_word(bits, v0);
+        tmem_st8(taddr(tbase, q * 32, col), v0);
+        pa += __popc(bits & valid(rem));
+      }
+    }
+#pragma unroll
+    for (int it = tid; it < 4 * BN; it += kThreads) {  // B: (column n, word u)
+      const int n = it % BN, u = it / BN;
+      uint32_t w = *reinterpret_cast<const uint32_t*>(stg + (128 + n) * 16 + 4 * u);
+      const int rem = p.K - 32 * (4 * s + u);  // valid bits of this word
+      if (rem < 32) w &= rem > 0 ? (1u << rem) - 1u : 0u;
+      if (n0 + n >= p.N) w = 0u;
+      uint32_t o[8];
+      expand_word01(w, o);
+      uint8_t* dst = bring + (size_t)r * L::kBSlot + (n >> 3) * 1024 + (2 * u) * 128 + (n & 7) * 16;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+      *reinterpret_cast<uint4*>(dst + 128) = make_uint4(o[4], o[5], o[6], o[7]);
+    }
+    tmem_st_wait();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B read by the tensor core
+    fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+      const uint64_t b0 = sdesc(smem_u32(bring + (size_t)r * L::kBSlot), 128, 1024);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        mma_i8_ts(tbase, tbase + BN + r * 32 + 8 * j, b0 + (uint64_t)(16 * j), idesc, (s | j) != 0);
+      mma_commit(&mma_done[r]);
+      if (s == KS - 1) mma_commit(&acc_done);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  pa_sh[h][q * 32 + lane] = pa;
+  mbar_wait(&acc_done, 0);
+  fence_after();
+  __syncthreads();
+  // ---- epilogue: warp (q, h) reads lane quarter q; v = kv - 2 d ----
+  const int rr0 = q * 32 + lane, row = m0 + rr0;
+  int kv = p.K;
+#pragma unroll
+  for (int j = 0; j < kHG; ++j) kv -= 2 * pa_sh[j][rr0];
+  if (p.mode == EPI_BITS) {
+#pragma unroll 1
+    for (int c0 = h * (BN / kHG); c0 < (h + 1) * (BN / kHG); c0 += 16) {
+      uint32_t acc[16];
+      tmem_ld16(taddr(tbase, q * 32, c0), acc);
+      tmem_ld_wait();
+      const int ncol = min(16, p.N - (n0 + c0));
+      if (row < p.M && ncol > 0) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int2 t = thr[c0 + j];
+          word |= (uint32_t)((uint32_t)(kv - 2 * (int)acc[j] - t.x) <= (uint32_t)t.y) << j;
+        }
+        if (ncol < 16) word &= (1u << ncol) - 1u;
+        reinterpret_cast<uint16_t*>(p.out_bits)[(size_t)row * p.cwo32 * 2 + (n0 + c0) / 16] = (uint16_t)word;
+      }
+    }
+  } else {
+    // 64-column halves staged through shared memory (the rings are dead), then row-contiguous
+    // stores: int32 rows at a 272-byte pitch, f64 rows at a 528-byte pitch
+#pragma unroll 1
+    for (int hb = 0; hb < BN / 64; ++hb) {
+      constexpr int kCW = 64 / kHG;  // this warp's columns of the half: c0 .. c0 + kCW - 1
+      const int c0 = hb * 64 + h * kCW;
+      uint32_t acc[kCW];
+#pragma unroll
+      for (int j = 0; j < kCW; j += 16) tmem_ld16(taddr(tbase, q * 32, c0 + j), acc + j);
+      tmem_ld_wait();
+      if (p.mode == EPI_F64) {
+        constexpr int kPitch = 66;
+        double* st = reinterpret_cast<double*>(smem);
+#pragma unroll
+        for (int j = 0; j < kCW; j += 2) {
+          double2 y;
+          y.x = bn_apply((double)(kv - 2 * (int)acc[j]), bnp[0][c0 + j], bnp[1][c0 + j], bnp[2][c0 + j],
+                         bnp[3][c0 + j], bnp[4][c0 + j]);
+          y.y = bn_apply((double)(kv - 2 * (int)acc[j + 1]), bnp[0][c0 + j + 1], bnp[1][c0 + j + 1],
+                         bnp[2][c0 + j + 1], bnp[3][c0 + j + 1], bnp[4][c0 + j + 1]);
+          *reinterpret_cast<double2*>(st + rr0 * kPitch + h * kCW + j) = y;
+        }
+        __syncthreads();
+        const int nb = n0 + hb * 64;
+        const bool vec = (p.N & 1) == 0 && nb + 64 <= p.N;
+        for (int rr = warp; rr < 128; rr += kThreads / 32) {
+          const int orow = m0 + rr;
+          if (orow >= p.M) break;
+          const int cc = lane * 2;
+          double* dst = p.rout + (size_t)orow * p.N + nb + cc;
+          const double2 v = *reinterpret_cast<const double2*>(st + rr * kPitch + cc);
+          if (vec) {
+            *reinterpret_cast<double2*>(dst) = v;
+          } else {
+            if (nb + cc < p.N) dst[0] = v.x;
+            if (nb + cc + 1 < p.N) dst[1] = v.y;
+          }
+        }
+      } else {
+        constexpr int kPitch = 68;
+        int32_t* st = reinterpret_cast<int32_t*>(smem);
+        // raw = popc(a ^ b) = (K - v) / 2
+        const int m2 = p.raw ? 1 : -2, c2 = p.raw ? (p.K - kv) / 2 : kv;
+#pragma unroll
+        for (int j = 0; j < kCW; j += 4) {
+          int4 v;
+          v.x = c2 + m2 * (int)acc[j];
+          v.y = c2 + m2 * (int)acc[j + 1];
+          v.z = c2 + m2 * (int)acc[j + 2];
+          v.w = c2 + m2 * (int)acc[j + 3];
+          *reinterpret_cast<int4*>(st + rr0 * kPitch + h * kCW + j) = v;
+        }
+        __syncthreads();
+        const int nb = n0 + hb * 64;
+        const bool vec = (p.N & 3) == 0 && nb + 64 <= p.N;
+        for (int rr = warp * 2 + (lane >> 4); rr < 128; rr += 2 * (kThreads / 32)) {
+          const int orow = m0 + rr;
+          if (orow >= p.M) break;
+          const int cc = (lane & 15) * 4;
+          int32_t* dst = p.out + (size_t)orow * p.N + nb + cc;
+          const int4 v = *reinterpret_cast<const int4*>(st + rr * kPitch + cc);
+          if (vec) {
+            *reinterpret_cast<int4*>(dst) = v;
+          } else {
+            const int vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (nb + cc + k < p.N) dst[k] = vv[k];
+          }
+        }
+      }
+      __syncthreads();  // the staging area is reused by the next half
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tbase, L::kTmemCols);
+}
+
+static BmmTcArgs bmm_args(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e) {
+  BmmTcArgs p{};
+  p.a = a;
+  p.b = b;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.Kp = (K + 127) / 128 * 128;
+  p.mode = e.mode;
+  p.raw = e.raw;
+  p.out = e.out_i32;
+  p.out_bits = reinterpret_cast<uint32_t*>(e.out_bits);
+  p.cwo32 = (N + 127) / 128 * 4;
+  p.thr_lo = e.thr_lo;
+  p.thr_hi = e.thr_hi;
+  p.rout = e.rout;
+  p.bn_mean = e.bn_mean;
+  p.bn_s = e.bn_s;
+  p.bn_rcp = e.bn_rcp;
+  p.bn_gamma = e.bn_gamma;
+  p.bn_beta = e.bn_beta;
+  return p;
+}
+
+template <int BN>
+static void launch_bmm_pipe_bn(const BmmTcArgs& p, cudaStream_t st) {
+  static thread_local int configured = -1;
+  int dev = 0;
+  BT_CUDA(cudaGetDevice(&dev));
+  if (configured != dev) {
+    BT_CUDA(cudaFuncSetAttribute(bmm_pipe_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 bmmp::Smem<BN>::kBytes));
+    configured = dev;
+  }
+  const dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + 127) / 128));
+  bmm_pipe_kernel<BN><<<grid, bmmp::Smem<BN>::kThreads, bmmp::Smem<BN>::kBytes, st>>>(p);
+  BT_CUDA(cudaGetLastError());
+  note_tc_launch(p.mode == EPI_BITS ? "bmm_pipe/bin" : p.mode == EPI_F64 ? "bmm_pipe/bn" : "bmm_pipe/i32",
+                 (int)(grid.x * grid.y), (int)(grid.x * grid.y));
+}
+
+// Any M, N, K: 128 x 256 tiles (one CTA per SM, N = 256 MMAs) when they fill every SM at least
+// twice, else 128 x 128 tiles when they fill the two CTA slots per SM, else 128 x 64.
+void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
+  const BmmTcArgs p = bmm_args(M, N, K, a, b, e);
+  int dev = 0, sms = 148;
+  BT_CUDA(cudaGetDevice(&dev));
+  BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long mt = (M + 127) / 128;
+  if (mt * ((N + 255) / 256) >= 2LL * sms) launch_bmm_pipe_bn<256>(p, st);
+  else if (mt * ((N + 127) / 128) >= 2LL * sms) launch_bmm_pipe_bn<128>(p, st);
+  else launch_bmm_pipe_bn<64>(p, st);
+}
+
+static std::atomic<int> g_bmm_kernel{BTNN_BMM_AUTO};
+
+// Packed-operand BMM: the whole-K kernel when K fits it, else the K-pipelined one
+// (btnn_cuda_set_bmm_kernel forces either).
+const char* launch_bmm_packed(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e,
+                              cudaStream_t st) {
+  const int k = g_bmm_kernel.load();
+  const bool whole = k == BTNN_BMM_WHOLE_K || (k == BTNN_BMM_AUTO && bmm_tc_supported(M, N, K));
+  if (whole) {
+    require(bmm_tc_supported(M, N, K), BTNN_UNSUPPORTED_SHAPE, "whole-K BMM kernel: K > 1536");
+    launch_bmm_tc(M, N, K, a, b, e, st);
+    return "tc_i8_bmm";
+  }
+  launch_bmm_pipe(M, N, K, a, b, e, st);
+  return "tc_i8_bmm_pipe";
+}
+
+// Fully-connected plan layers: the packed kernels when K fits the whole-K one, or when the
+// pipelined one has at least one 128 x 64 tile per SM; nullptr leaves the layer to the
+// split-K implicit GEMM (few output tiles, long K).
+const char* launch_bmm_fc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
+  const int k = g_bmm_kernel.load();
+  if (k != BTNN_BMM_PIPELINED && bmm_tc_supported(M, N, K)) {
+    launch_bmm_tc(M, N, K, a, b, e, st);
+    return "tc_i8_bmm";
+  }
+  int dev = 0, sms = 148;
+  BT_CUDA(cudaGetDevice(&dev));
+  BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long long tiles = (long long)((M + 127) / 128) * ((N + 63) / 64);
+  if (k == BTNN_BMM_PIPELINED || (k == BTNN_BMM_AUTO && tiles >= sms)) {
+    launch_bmm_pipe(M, N, K, a, b, e, st);
+    return "tc_i8_bmm_pipe";
+  }
+  return nullptr;
+}
+
 }  // namespace btnn_gpu
+
+extern "C" int btnn_cuda_set_bmm_kernel(int which) {
+  return btnn_gpu::guard([&] {
+    btnn_gpu::require(which >= BTNN_BMM_AUTO && which <= BTNN_BMM_PIPELINED, BTNN_INVALID_INPUT,
+                      "set_bmm_kernel: unknown kernel");
+    btnn_gpu::g_bmm_kernel.store(which);
+  });
+}
 
 extern "C" int btnn_cuda_debug_bmm_timestamps(unsigned long long* out, size_t n) {
   return btnn_gpu::guard([&] {

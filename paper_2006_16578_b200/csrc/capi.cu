@@ -243,13 +243,10 @@ static const char* run_gemm(const ConvShape& s0, const uint64_t* act, const uint
   return launch_bgemm(s, act, filt, e, st, EngineHint::Auto, tc ? &tcf : nullptr);
 }
 
-// Kernel-level BMM (bmm.hpp:204-274): the one-kernel packed-operand GEMM when the inner
-// dimension fits it (bmm_tc.cu), else the implicit-GEMM path with B expanded for the call.
+// Kernel-level BMM (bmm.hpp:204-274): one tensor-core kernel on the packed operands
+// (bmm_tc.cu: whole-K or K-pipelined); the CUDA-core engine when forced.
 static const char* run_bmm(const ConvShape& s, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
-  if (engine_override() != BTNN_ENGINE_POPC && bmm_tc_supported(s.N, s.O, s.C)) {
-    launch_bmm_tc(s.N, s.O, s.C, a, b, e, st);
-    return "tc_i8";
-  }
+  if (engine_override() != BTNN_ENGINE_POPC) return launch_bmm_packed(s.N, s.O, s.C, a, b, e, st);
   return run_gemm(s, a, b, e, st);
 }
 

@@ -43,10 +43,8 @@ const char* launch_bgemm(const ConvShape& s, const uint64_t* act, const uint64_t
     // (bmm_tc.cu) from the RowPacked activations and the ColPacked weights — threshold bits or
     // the last layer's bn logits
     const bool fc = s.P == 1 && s.Q == 1 && s.KH == 1 && s.KW == 1 && s.pad == 0 && !e.rin && !e.rout_half && !e.pool;
-    if (fc && bmm_tc_supported(s.N, s.O, s.C) &&
-        ((e.mode == EPI_BITS && !e.bn_mean && e.out_bits) || (e.mode == EPI_F64 && e.bn_mean && e.rout))) {
-      launch_bmm_tc(s.N, s.O, s.C, act, filt, e, st);
-      return "tc_i8_bmm";
+    if (fc && ((e.mode == EPI_BITS && !e.bn_mean && e.out_bits) || (e.mode == EPI_F64 && e.bn_mean && e.rout))) {
+      if (const char* used = launch_bmm_fc(s.N, s.O, s.C, act, filt, e, st)) return used;
     }
     return launch_bgemm_tc(s, act, *tc, e, st, ch) ? "tc_i8_splitk" : "tc_i8";
   }

@@ -20,4 +20,12 @@ __device__ __forceinline__ void expand_word(uint32_t w, uint32_t* o) {
   for (int s = 0; s < 8; ++s) o[s] = prmt_sign(w << s) | 0x01010101u;
 }
 
+// 32 bits -> 8 words of 4 {0,1} bytes in the same K order as expand_word: byte k of word s =
+// bit 8k + 7 - s. Paired with a +-1 operand, sum(a * b01) = sum over b's set bits of a, and
+// the +-1 dot follows as sum(a) - 2 sum(a * b01).
+__device__ __forceinline__ void expand_word01(uint32_t w, uint32_t* o) {
+#pragma unroll
+  for (int s = 0; s < 8; ++s) o[s] = (w >> (7 - s)) & 0x01010101u;
+}
+
 }  // namespace btnn_gpu

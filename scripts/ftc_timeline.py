@@ -26,9 +26,7 @@ print("tile: bstart bfree bdone | mma_start mma_issued | epi_start epi_done  (cl
 for i in range(40):
     print(i, (t[i, :7] - t0).tolist())
 
-e = ts[512:640].astype(np.int64).reshape(8, 16)
-print("epilogue warp 0 per channel half: [acc wait, process, tap store] (clk)")
+e = ts[512:640].astype(np.int64).reshape(8, 2, 8)
+print("epilogue warp 0, tiles 20..27, per group: acc-wait | ld | process | ld | process | tap store | bits (clk)")
 for i in range(8):
-    r = e[i]
-    print(i + 4, [[int(r[1 + 3 * h] - (r[0] if h == 0 else r[3 * h])), int(r[2 + 3 * h] - r[1 + 3 * h]),
-                   int(r[3 + 3 * h] - r[2 + 3 * h])] for h in range(2)])
+    print(i + 20, [np.diff(e[i, g, :7]).tolist() for g in range(2)], "gap to next group", int(e[i, 1, 0] - e[i, 0, 6]))

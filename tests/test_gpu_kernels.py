@@ -70,9 +70,9 @@ def test_bmm_1024_cube():
 
 @pytest.mark.parametrize("m,n,k", [(300, 700, 1536), (1000, 65, 1200), (129, 1, 33), (1, 129, 1408), (130, 131, 1537)])
 def test_bmm_packed_kernel_shapes(m, n, k, engine):
-    """The one-kernel packed BMM (bmm_tc.cu) over tile edges in M and N, inner dimensions up to
-    its 1536-bit limit (partial last words, odd chunk counts), and past it (the implicit-GEMM
-    path): pm1, raw and thresholded bits vs the C oracle."""
+    """The whole-K packed BMM (bmm_tc.cu) over tile edges in M and N, inner dimensions up to
+    its 1536-bit limit (partial last words, odd chunk counts), and past it (the K-pipelined
+    kernel): pm1, raw and thresholded bits vs the C oracle."""
     rng = np.random.default_rng(m * 7 + n * 3 + k)
     fa, fb = rng.standard_normal(m * k, dtype=np.float32), rng.standard_normal(k * n, dtype=np.float32)
     A, Bw = Wt.pack_matrix(fa, m, k, capi.ROW_PACKED), Wt.pack_matrix(fb, k, n, capi.COL_PACKED)
@@ -82,7 +82,7 @@ def test_bmm_packed_kernel_shapes(m, n, k, engine):
                         ptr(want, C.c_int32))
     assert np.array_equal(B.bmm_pm1(da, A, db, Bw).reshape(-1), want), (m, n, k)
     if engine == "tc":
-        assert capi.last_tc_launch()[0] == ("bmm_packed/i32" if k <= 1536 else "tmemA/i32"), capi.last_tc_launch()
+        assert capi.last_tc_launch()[0] == ("bmm_packed/i32" if k <= 1536 else "bmm_pipe/i32"), capi.last_tc_launch()
     if k % 128 == 0:
         assert np.array_equal(k - 2 * B.bmm_raw(da, A, db, Bw).reshape(-1), want)
     bits = B.bmm_pm1_bin(da, A, db, Bw)
@@ -91,6 +91,61 @@ def test_bmm_packed_kernel_shapes(m, n, k, engine):
     for j in range(n):
         words[:, j // 64] |= dense[:, j].astype(np.uint64) << np.uint64(j % 64)
     assert np.array_equal(np.asarray(bits).reshape(-1), words.reshape(-1))
+
+
+@pytest.fixture
+def pipelined():
+    capi.set_bmm_kernel(capi.BMM_PIPELINED)
+    yield
+    capi.set_bmm_kernel(capi.BMM_AUTO)
+
+
+@pytest.mark.parametrize("i", indices(load("bmm"), "s", "shape"))
+def test_bmm_golden_pipelined(i, pipelined, engine):
+    """The reference's BMM golden cases (plain and fsb, four threshold kinds) on the K-pipelined kernel."""
+    test_bmm_golden(i)
+    if engine == "tc":
+        assert capi.last_tc_launch()[0].startswith("bmm_pipe/"), capi.last_tc_launch()
+
+
+def test_bmm_random_sweep_pipelined(pipelined):
+    test_bmm_random_sweep_vs_oracle()
+
+
+@pytest.mark.parametrize("m,n,k", [(300, 700, 1536), (129, 1, 33), (1, 129, 1408), (130, 131, 1537), (257, 300, 4160),
+                                   (1024, 1100, 9216), (512, 512, 25088), (96, 2000, 4097), (8192, 1200, 300)])
+def test_bmm_pipelined_shapes(m, n, k, pipelined, engine):
+    """K-pipelined packed BMM: tile edges in M and N (128 x 64 and 128 x 128 tiles), K-step
+    counts below and above the ring and prefetch depths, partial last words; pm1, raw and
+    thresholded bits (random tau, all four kinds) vs the C oracle."""
+    rng = np.random.default_rng(m * 5 + n * 11 + k)
+    wpr = (k + 127) // 128 * 2  # words per packed row / column; bits past K are zero
+
+    def packed(rows):
+        w = rng.integers(0, 2**64, (rows, wpr), dtype=np.uint64)
+        bit = np.arange(wpr * 64).reshape(wpr, 64)
+        keep = (np.uint64(1) << np.arange(64, dtype=np.uint64))[None, :] * (bit < k)
+        w &= np.bitwise_or.reduce(keep.astype(np.uint64), axis=1)[None, :]
+        return w.reshape(-1)
+
+    A, Bw = packed(m), packed(n)
+    da, db = md(m, k, capi.ROW_PACKED), md(k, n, capi.COL_PACKED)
+    want = np.zeros(m * n, dtype=np.int32)
+    assert oracle().bo_bmm_pm1(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64), capi.BMM_NAIVE,
+                               ptr(want, C.c_int32)) == 0
+    assert np.array_equal(B.bmm_pm1(da, A, db, Bw).reshape(-1), want), (m, n, k)
+    if engine == "tc":
+        assert capi.last_tc_launch()[0].startswith("bmm_pipe") and capi.last_tc_launch()[0].endswith("/i32")
+    if k % 128 == 0:  # (bmm_raw: the reference requires whole 128-bit words)
+        assert np.array_equal(B.bmm_raw(da, A, db, Bw).reshape(-1), (k - want) // 2)
+    tau = rng.standard_normal(n) * 30
+    kind = rng.integers(0, 4, n).astype(np.uint8)
+    bits = B.bmm_pm1_bin(da, A, db, Bw, tau=tau, kind=kind)
+    wbits = np.zeros_like(bits)
+    assert oracle().bo_bmm_pm1_bin(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64), capi.BMM_NAIVE,
+                                   ptr(np.ascontiguousarray(tau), C.c_double), ptr(kind, C.c_uint8), n,
+                                   ptr(wbits, C.c_uint64)) == 0
+    assert np.array_equal(bits, wbits)
 
 
 @pytest.mark.parametrize("i", indices(load("bconv"), "c", "case"))

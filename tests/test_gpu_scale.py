@@ -68,7 +68,7 @@ def _assert_launch(expect, exclude=()):
         assert part in variant.split("/"), (variant, expect)
     for part in exclude:
         assert part not in variant.split("/"), (variant, exclude)
-    if not variant.startswith("bmm_packed"):  # (one tile per CTA by design: not persistent)
+    if not variant.startswith(("bmm_packed", "bmm_pipe")):  # (one tile per CTA by design: not persistent)
         assert units >= 3 * grid, f"{variant}: {units} units on {grid} CTAs — fewer than 3 per CTA"
     return variant
 
@@ -127,11 +127,13 @@ def test_tc_variant_many_tiles_per_cta(case):
         capi.set_engine(capi.ENGINE_AUTO)
 
 
-@pytest.mark.parametrize("kk,kind_", [(1024, "bmm_packed"), (2048, "tmemA")])
-def test_bmm_many_tiles_per_cta(kk, kind_):
-    """BMM 8192 x K x 1024 packed -> int32 and -> thresholded bits: K = 1024 runs the one-kernel
-    packed BMM (1024 CTAs), K = 2048 the implicit GEMM with 512 tiles over the persistent CTAs."""
+@pytest.mark.parametrize("kk,kind_,force", [(1024, "bmm_packed", 0), (2048, "bmm_pipe", 0), (1024, "bmm_pipe", 2)])
+def test_bmm_many_tiles_per_cta(kk, kind_, force):
+    """BMM 8192 x K x 1024 packed -> int32 and -> thresholded bits: K = 1024 runs the whole-K
+    packed BMM (1024 CTAs), K = 2048 the K-pipelined one (512 128 x 128 tiles, two CTAs per SM),
+    and K = 1024 forced onto the pipelined kernel."""
     capi.set_engine(capi.ENGINE_TC)
+    capi.set_bmm_kernel(force)
     try:
         rng = np.random.default_rng(9)
         m, nn = 8192, 1024
@@ -147,7 +149,7 @@ def test_bmm_many_tiles_per_cta(kk, kind_):
         tau = rng.standard_normal(nn) * 20
         kind = rng.integers(0, 4, nn).astype(np.uint8)
         bits = B.bmm_pm1_bin(da, A, db, Bw, tau=tau, kind=kind)
-        _assert_launch((kind_, "bin" if kind_ == "bmm_packed" else "thr"))
+        _assert_launch((kind_, "bin"))
         wbits = np.zeros_like(bits)
         assert oracle().bo_bmm_pm1_bin(C.byref(da), ptr(A, C.c_uint64), C.byref(db), ptr(Bw, C.c_uint64),
                                        capi.BMM_BLOCKED, ptr(np.ascontiguousarray(tau), C.c_double),
@@ -155,6 +157,7 @@ def test_bmm_many_tiles_per_cta(kk, kind_):
         assert np.array_equal(bits, wbits)
     finally:
         capi.set_engine(capi.ENGINE_AUTO)
+        capi.set_bmm_kernel(capi.BMM_AUTO)
 
 
 def _ref_run(m, ws, x):
