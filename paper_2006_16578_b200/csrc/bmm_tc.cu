@@ -361,82 +361,71 @@ void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, co
 }
 
 // ---------------------------------------------------------------------------------------------
-// K-pipelined variant for any inner dimension (bmm_pipe_kernel<BN>): 128 x BN output tiles,
-// 8 warps, up to two CTAs per SM. Per K-step of 128 bits:
-//   * one 16-byte cp.async per A row / B column stages the packed bits kPD steps ahead;
-//   * all warps expand step s — A row by row to +-1 bytes into a TMEM ring slot (tcgen05.st,
-//     32 columns), B to {0,1} bytes (bit set -> 1, bits past K -> 0; two instructions per
-//     output word instead of three) into a shared-memory ring slot (canonical K-major, 8 core
-//     columns of 16 B per 8-column group) — while the MMAs of step s - 1 run; the A threads
-//     also count their row's set bits below K (pa);
-//   * thread 0 issues the step's four M128 x BN x K32 kind::i8 MMAs (A from TMEM) and commits
-//     them to the slot's mbarrier, which the expansion of step s + kR waits for.
-// The accumulator holds d = sum(a * b01) over K; the +-1 dot is v = sum(a) - 2 d =
-// K - 2 pa - 2 d, read once at the end by the same epilogues as bmm_tc_kernel (int32 /
-// thresholded bits / exact bn logits).
+// K-pipelined variant for any inner dimension (bmm_pipe_kernel<BN>): one 128 x BN output tile
+// per CTA (two CTAs per SM for BN <= 128, one for BN = 256), warp-specialized, per K-step of
+// 128 bits:
+//   * A warps (4 or 8; TMEM lane quarter = warp % 4): each thread stages its row's 16 bytes
+//     (or half of them) with its own cp.async kPD steps ahead, expands them to +-1 bytes and
+//     stores them into the step's TMEM ring slot (tcgen05.st), counting the row's set bits
+//     below K (pa);
+//   * B warps (4 or 8): each thread stages one column's 16 bytes (or half) the same way and
+//     expands them to {0,1} bytes (bit set -> 1, bits past K -> 0: two instructions per output
+//     word) into the step's shared-memory ring slot (canonical K-major, 8 core columns of 16 B
+//     per 8-column group);
+//   * one MMA warp waits for both halves of a slot, issues the four M128 x BN x K32 kind::i8
+//     MMAs (A from TMEM) and commits them to the slot's empty barrier.
+// No thread waits for another thread's staging: the only cross-warp handshakes are the ring's
+// full / empty mbarriers. The accumulator holds d = sum(a * b01); the +-1 dot is
+// v = sum(a) - 2 d = K - 2 pa - 2 d, read at the end by all producer warps with the epilogues of
+// bmm_tc_kernel (int32 / thresholded bits / exact bn logits).
 namespace bmmp {
 constexpr int kR = 4;          // ring depth: expanded B slots (smem) and A slots (TMEM)
 constexpr int kPD = 4;         // packed-bit prefetch distance in K-steps
-constexpr int kPS = kPD + 1;   // packed staging slots
+constexpr int kPS = kPD + 1;   // packed staging slots per thread
 template <int BN>
-struct Smem {
-  // 8 warps (16 for BN = 256, one CTA per SM); TMEM: BN accumulator + kR x 32 A columns
-  static constexpr int kThreads = BN == 256 ? 512 : 256;
-  static constexpr int kHG = kThreads / 128;  // warps per TMEM lane quarter
-  static constexpr int kTmemCols = BN == 256 ? 512 : 256;
-  static constexpr int kStage = (128 + BN) * 16;  // packed bits of one K-step
-  static constexpr int kBSlot = BN * 128;         // expanded B of one K-step
-  static constexpr int kOffStage = kR * kBSlot;
-  static constexpr int kMain = kOffStage + kPS * kStage;
-  static constexpr int kEpi = 128 * 68 * 8;       // epilogue staging: 128 rows x 64 columns
+struct Cfg {
+  static constexpr int kAW = BN == 256 ? 8 : 4;            // A warps
+  static constexpr int kBW = BN == 256 ? 8 : 4;            // B warps
+  static constexpr int kEW = kAW + kBW;                    // epilogue warps (all producers)
+  static constexpr int kHG = kEW / 4;                      // epilogue warps per lane quarter
+  static constexpr int kThreads = 32 * (kEW + 1);          // + the MMA warp
+  static constexpr int kAWords = 4 * 4 / kAW;              // A words per thread per K-step
+  static constexpr int kBWords = 4 * BN / (32 * kBW);      // B words per thread per K-step
+  static constexpr int kTmemCols = BN == 256 ? 512 : 256;  // BN accumulator + kR x 32 A columns
+  static constexpr int kBSlot = BN * 128;                  // expanded B of one K-step
+  static constexpr int kOffStage = kR * kBSlot;            // per-thread packed staging
+  static constexpr int kMain = kOffStage + kPS * 32 * kEW * 16;
+  static constexpr int kEpi = 128 * 68 * 8;                // epilogue staging: 128 x 64 columns
+  static constexpr int kMax = kMain > kEpi ? kMain : kEpi;
   // >= 80 KB: at most two CTAs per SM, so their TMEM allocations always fit
-  static constexpr int kBytes = (kMain > kEpi ? kMain : kEpi) > 80 * 1024 ? (kMain > kEpi ? kMain : kEpi) : 80 * 1024;
+  static constexpr int kBytes = kMax > 80 * 1024 ? kMax : 80 * 1024;
 };
 }  // namespace bmmp
 
 template <int BN>
-__global__ void __launch_bounds__(bmmp::Smem<BN>::kThreads, BN == 256 ? 1 : 2)
+__global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
     bmm_pipe_kernel(const __grid_constant__ BmmTcArgs p) {
   using namespace umma;
-  using L = bmmp::Smem<BN>;
-  constexpr int kThreads = L::kThreads, kHG = L::kHG, kWA = 4 / kHG;  // A words per thread
+  using L = bmmp::Cfg<BN>;
+  constexpr int kThreads = L::kThreads, kHG = L::kHG, kR = bmmp::kR, kPD = bmmp::kPD, kPS = bmmp::kPS;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t mma_done[bmmp::kR];
-  __shared__ uint64_t acc_done;
+  __shared__ uint64_t full_a[kR], full_b[kR], empty[kR], acc_done;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int2 thr[BN];
   __shared__ double bnp[5][BN];
-  __shared__ int pa_sh[kHG][128];  // per A row: set bits below K, per word share
+  __shared__ int pa_sh[L::kAW / 4][128];  // per A row: set bits below K, per word share
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q = warp & 3, h = warp >> 2;  // TMEM lane quarter, share of the work
-  int pa = 0;
   const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
   const int KS = p.Kp / 128;  // K-steps = 16-byte chunks per packed row
   uint8_t* bring = smem;
-  uint8_t* stage = smem + L::kOffStage;
   const uint8_t* ga = reinterpret_cast<const uint8_t*>(p.a);
   const uint8_t* gb = reinterpret_cast<const uint8_t*>(p.b);
-  // packed bits of K-step s -> staging slot s % kPS (threads 0-127: A rows, 128-: B columns);
-  // every thread commits a group per call, so group counts stay uniform
-  auto issue = [&](int s) {
-    if (s < KS) {
-      uint8_t* dst = stage + (size_t)(s % bmmp::kPS) * L::kStage;
-      if (tid < 128) {
-        const int row = m0 + tid;
-        const bool ok = row < p.M;
-        cp_async16(smem_u32(dst + tid * 16), ga + ((size_t)(ok ? row : 0) * KS + s) * 16, ok ? 16 : 0);
-      } else if (tid < 128 + BN) {
-        const int col = n0 + tid - 128;
-        const bool ok = col < p.N;
-        cp_async16(smem_u32(dst + tid * 16), gb + ((size_t)(ok ? col : 0) * KS + s) * 16, ok ? 16 : 0);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-#pragma unroll
-  for (int s = 0; s < bmmp::kPD; ++s) issue(s);
   if (tid == 0) {
-    for (int r = 0; r < bmmp::kR; ++r) mbar_init(&mma_done[r], 1);
+    for (int r = 0; r < kR; ++r) {
+      mbar_init(&full_a[r], L::kAW);
+      mbar_init(&full_b[r], L::kBW);
+      mbar_init(&empty[r], 1);
+    }
     mbar_init(&acc_done, 1);
     fence_mbar_init();
   }
@@ -465,121 +454,198 @@ __global__ void __launch_bounds__(bmmp::Smem<BN>::kThreads, BN == 256 ? 1 : 2)
   __syncthreads();
   fence_after();
   const uint32_t tbase = tmem_base_sh;
-  const uint32_t idesc = idesc_i8(128, BN);
-  for (int s = 0; s < KS; ++s) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(bmmp::kPD - 1) : "memory");
-    __syncthreads();  // step s staged by every thread; step s - 1's staging slot fully read
-    issue(s + bmmp::kPD);
-    const int r = s % bmmp::kR;
-    if (s >= bmmp::kR) mbar_wait(&mma_done[r], (uint32_t)((s / bmmp::kR - 1) & 1));  // ring slot free
-    const uint8_t* stg = stage + (size_t)(s % bmmp::kPS) * L::kStage;
-    {  // A: row q*32 + lane, 32-bit words kWA*h .. of the step -> 8 TMEM columns each
-      const uint32_t col = (uint32_t)(BN + r * 32 + 8 * kWA * h);
-      const int rem = p.K - 32 * (4 * s + kWA * h);  // valid bits of the first word
-      auto valid = [](int r_) { return r_ >= 32 ? ~0u : r_ > 0 ? (1u << r_) - 1u : 0u; };
-      if constexpr (kWA == 2) {
-        const uint2 bits = *reinterpret_cast<const uint2*>(stg + (q * 32 + lane) * 16 + 8 * h);
-        uint32_t v0[8], v1[8];
-        expand_word(bits.x, v0);
-        expand_word(bits.y, v1);
-        tmem_st8(taddr(tbase, q * 32, col), v0);
-        tmem_st8(taddr(tbase, q * 32, col + 8), v1);
-        pa += __popc(bits.x & valid(rem)) + __popc(bits.y & valid(rem - 32));
-      } else {
-        const uint32_t bits = *reinterpret_cast<const uint32_t*>(stg + (q * 32 + lane) * 16 + 4 * h);
-        uint32_t v0[8];
-        expand_word(bits, v0);
-        tmem_st8(taddr(tbase, q * 32, col), v0);
-        pa += __popc(bits & valid(rem));
+  int pa = 0;
+  auto valid = [](int r_) { return r_ >= 32 ? ~0u : r_ > 0 ? (1u << r_) - 1u : 0u; };
+  if (warp < L::kAW) {
+    // ================= A producers: row q*32 + lane, words ag*kAWords .. of each K-step =================
+    const int q = warp & 3, ag = warp >> 2, row = q * 32 + lane;
+    constexpr int NWd = L::kAWords;
+    const bool ok = m0 + row < p.M;
+    const uint8_t* src = ga + (size_t)(ok ? m0 + row : 0) * KS * 16 + ag * NWd * 4;
+    uint8_t* stg = smem + L::kOffStage + (size_t)tid * kPS * 16;
+    auto issue = [&](int s) {
+      if (s < KS) {
+        if constexpr (NWd == 4) cp_async16(smem_u32(stg + (s % kPS) * 16), src + (size_t)s * 16, ok ? 16 : 0);
+        else asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stg + (s % kPS) * 16)),
+                          "l"(src + (size_t)s * 16), "r"(ok ? 8 : 0) : "memory");
       }
-    }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 #pragma unroll
-    for (int it = tid; it < 4 * BN; it += kThreads) {  // B: (column n, word u)
-      const int n = it % BN, u = it / BN;
-      uint32_t w = *reinterpret_cast<const uint32_t*>(stg + (128 + n) * 16 + 4 * u);
-      const int rem = p.K - 32 * (4 * s + u);  // valid bits of this word
-      if (rem < 32) w &= rem > 0 ? (1u << rem) - 1u : 0u;
-      if (n0 + n >= p.N) w = 0u;
-      uint32_t o[8];
-      expand_word01(w, o);
-      uint8_t* dst = bring + (size_t)r * L::kBSlot + (n >> 3) * 1024 + (2 * u) * 128 + (n & 7) * 16;
-      *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
-      *reinterpret_cast<uint4*>(dst + 128) = make_uint4(o[4], o[5], o[6], o[7]);
+    for (int s = 0; s < kPD; ++s) issue(s);
+    for (int s = 0; s < KS; ++s) {
+      issue(s + kPD);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPD) : "memory");
+      const int r = s % kR;
+      uint32_t w[NWd], v[8 * NWd];
+      if constexpr (NWd == 4) {
+        const uint4 b4 = *reinterpret_cast<const uint4*>(stg + (s % kPS) * 16);
+        w[0] = b4.x; w[1] = b4.y; w[2] = b4.z; w[3] = b4.w;
+      } else {
+        const uint2 b2 = *reinterpret_cast<const uint2*>(stg + (s % kPS) * 16);
+        w[0] = b2.x; w[1] = b2.y;
+      }
+      const int rem = p.K - 32 * (4 * s + ag * NWd);
+#pragma unroll
+      for (int i = 0; i < NWd; ++i) {
+        expand_word(w[i], v + 8 * i);
+        pa += __popc(w[i] & valid(rem - 32 * i));
+      }
+      if (s >= kR) mbar_wait(&empty[r], (uint32_t)((s / kR - 1) & 1));  // MMAs of step s - kR done
+      const uint32_t ta = taddr(tbase, q * 32, (uint32_t)(BN + r * 32 + 8 * ag * NWd));
+      if constexpr (NWd == 4) tmem_st32(ta, v);
+      else tmem_st16(ta, v);
+      tmem_st_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_a[r]);
     }
-    tmem_st_wait();
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // B read by the tensor core
-    fence_before();
-    __syncthreads();
-    if (tid == 0) {
+    pa_sh[ag][row] = pa;
+  } else if (warp < L::kEW) {
+    // ================= B producers: column n, words bg*kBWords .. of each K-step =================
+    const int bt = tid - 32 * L::kAW;  // 0 .. 32*kBW - 1
+    constexpr int NWd = L::kBWords;
+    const int n = bt % BN, bg = bt / BN;
+    const bool ok = n0 + n < p.N;
+    const uint8_t* src = gb + (size_t)(ok ? n0 + n : 0) * KS * 16 + bg * NWd * 4;
+    uint8_t* stg = smem + L::kOffStage + (size_t)tid * kPS * 16;
+    auto issue = [&](int s) {
+      if (s < KS) {
+        if constexpr (NWd == 4) cp_async16(smem_u32(stg + (s % kPS) * 16), src + (size_t)s * 16, ok ? 16 : 0);
+        else asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stg + (s % kPS) * 16)),
+                          "l"(src + (size_t)s * 16), "r"(ok ? 8 : 0) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+#pragma unroll
+    for (int s = 0; s < kPD; ++s) issue(s);
+    for (int s = 0; s < KS; ++s) {
+      issue(s + kPD);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kPD) : "memory");
+      const int r = s % kR;
+      uint32_t w[NWd];
+      if constexpr (NWd == 4) {
+        const uint4 b4 = *reinterpret_cast<const uint4*>(stg + (s % kPS) * 16);
+        w[0] = b4.x; w[1] = b4.y; w[2] = b4.z; w[3] = b4.w;
+      } else {
+        const uint2 b2 = *reinterpret_cast<const uint2*>(stg + (s % kPS) * 16);
+        w[0] = b2.x; w[1] = b2.y;
+      }
+      const int rem = p.K - 32 * (4 * s + bg * NWd);
+      if (s >= kR) mbar_wait(&empty[r], (uint32_t)((s / kR - 1) & 1));
+      uint8_t* dst = bring + (size_t)r * L::kBSlot + (n >> 3) * 1024 + (n & 7) * 16;
+#pragma unroll
+      for (int i = 0; i < NWd; ++i) {
+        uint32_t o[8];
+        expand_word01(w[i] & valid(rem - 32 * i), o);
+        const int u = bg * NWd + i;  // word of the step: core columns 2u, 2u + 1
+        *reinterpret_cast<uint4*>(dst + (2 * u) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<uint4*>(dst + (2 * u + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // read by the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_b[r]);
+    }
+  } else {
+    // ================= MMA issuer =================
+    const uint32_t idesc = idesc_i8(128, BN);
+    for (int s = 0; s < KS; ++s) {
+      const int r = s % kR;
+      const uint32_t ph = (uint32_t)((s / kR) & 1);
+      mbar_wait(&full_a[r], ph);
+      mbar_wait(&full_b[r], ph);
       fence_after();
       const uint64_t b0 = sdesc(smem_u32(bring + (size_t)r * L::kBSlot), 128, 1024);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        mma_i8_ts(tbase, tbase + BN + r * 32 + 8 * j, b0 + (uint64_t)(16 * j), idesc, (s | j) != 0);
-      mma_commit(&mma_done[r]);
-      if (s == KS - 1) mma_commit(&acc_done);
+        mma_i8_ts_w(tbase, tbase + BN + r * 32 + 8 * j, b0 + (uint64_t)(16 * j), idesc, (s | j) != 0);
+      mma_commit_w(&empty[r]);
     }
+    mma_commit_w(&acc_done);
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  pa_sh[h][q * 32 + lane] = pa;
+  __syncthreads();  // pa_sh written
   mbar_wait(&acc_done, 0);
   fence_after();
-  __syncthreads();
-  // ---- epilogue: warp (q, h) reads lane quarter q; v = kv - 2 d ----
-  const int rr0 = q * 32 + lane, row = m0 + rr0;
-  int kv = p.K;
+  if (warp < L::kEW) {
+    // ---- epilogue: warp (q, h) reads lane quarter q; v = kv - 2 d ----
+    const int q = warp & 3, h = warp >> 2;
+    const int rr0 = q * 32 + lane, row = m0 + rr0;
+    int kv = p.K;
 #pragma unroll
-  for (int j = 0; j < kHG; ++j) kv -= 2 * pa_sh[j][rr0];
-  if (p.mode == EPI_BITS) {
+    for (int j = 0; j < L::kAW / 4; ++j) kv -= 2 * pa_sh[j][rr0];
+    if (p.mode == EPI_BITS) {
 #pragma unroll 1
-    for (int c0 = h * (BN / kHG); c0 < (h + 1) * (BN / kHG); c0 += 16) {
-      uint32_t acc[16];
-      tmem_ld16(taddr(tbase, q * 32, c0), acc);
-      tmem_ld_wait();
-      const int ncol = min(16, p.N - (n0 + c0));
-      if (row < p.M && ncol > 0) {
-        uint32_t word = 0;
+      for (int c0 = h * (BN / kHG); c0 < (h + 1) * (BN / kHG); c0 += 16) {
+        uint32_t acc[16];
+        tmem_ld16(taddr(tbase, q * 32, c0), acc);
+        tmem_ld_wait();
+        const int ncol = min(16, p.N - (n0 + c0));
+        if (row < p.M && ncol > 0) {
+          uint32_t word = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int2 t = thr[c0 + j];
-          word |= (uint32_t)((uint32_t)(kv - 2 * (int)acc[j] - t.x) <= (uint32_t)t.y) << j;
+          for (int j = 0; j < 16; ++j) {
+            const int2 t = thr[c0 + j];
+            word |= (uint32_t)((uint32_t)(kv - 2 * (int)acc[j] - t.x) <= (uint32_t)t.y) << j;
+          }
+          if (ncol < 16) word &= (1u << ncol) - 1u;
+          reinterpret_cast<uint16_t*>(p.out_bits)[(size_t)row * p.cwo32 * 2 + (n0 + c0) / 16] = (uint16_t)word;
         }
-        if (ncol < 16) word &= (1u << ncol) - 1u;
-        reinterpret_cast<uint16_t*>(p.out_bits)[(size_t)row * p.cwo32 * 2 + (n0 + c0) / 16] = (uint16_t)word;
       }
     }
-  } else {
+  }
+  if (p.mode != EPI_BITS) {
     // 64-column halves staged through shared memory (the rings are dead), then row-contiguous
-    // stores: int32 rows at a 272-byte pitch, f64 rows at a 528-byte pitch
+    // stores by the producer warps: int32 rows at a 272-byte pitch, f64 rows at a 528-byte pitch
+    constexpr int kEW = L::kEW, kCW = 64 / kHG;  // a warp's columns of the half
+    const int q = warp & 3, h = warp >> 2;
+    const int rr0 = q * 32 + lane;
+    int kv = p.K;
+    if (warp < kEW) {
+#pragma unroll
+      for (int j = 0; j < L::kAW / 4; ++j) kv -= 2 * pa_sh[j][rr0];
+    }
 #pragma unroll 1
     for (int hb = 0; hb < BN / 64; ++hb) {
-      constexpr int kCW = 64 / kHG;  // this warp's columns of the half: c0 .. c0 + kCW - 1
       const int c0 = hb * 64 + h * kCW;
-      uint32_t acc[kCW];
+      if (warp < kEW) {
+        uint32_t acc[kCW];
 #pragma unroll
-      for (int j = 0; j < kCW; j += 16) tmem_ld16(taddr(tbase, q * 32, c0 + j), acc + j);
-      tmem_ld_wait();
-      if (p.mode == EPI_F64) {
-        constexpr int kPitch = 66;
-        double* st = reinterpret_cast<double*>(smem);
+        for (int j = 0; j < kCW; j += 16) tmem_ld16(taddr(tbase, q * 32, c0 + j), acc + j);
+        tmem_ld_wait();
+        if (p.mode == EPI_F64) {
+          double* st = reinterpret_cast<double*>(smem);
 #pragma unroll
-        for (int j = 0; j < kCW; j += 2) {
-          double2 y;
-          y.x = bn_apply((double)(kv - 2 * (int)acc[j]), bnp[0][c0 + j], bnp[1][c0 + j], bnp[2][c0 + j],
-                         bnp[3][c0 + j], bnp[4][c0 + j]);
-          y.y = bn_apply((double)(kv - 2 * (int)acc[j + 1]), bnp[0][c0 + j + 1], bnp[1][c0 + j + 1],
-                         bnp[2][c0 + j + 1], bnp[3][c0 + j + 1], bnp[4][c0 + j + 1]);
-          *reinterpret_cast<double2*>(st + rr0 * kPitch + h * kCW + j) = y;
+          for (int j = 0; j < kCW; j += 2) {
+            double2 y;
+            y.x = bn_apply((double)(kv - 2 * (int)acc[j]), bnp[0][c0 + j], bnp[1][c0 + j], bnp[2][c0 + j],
+                           bnp[3][c0 + j], bnp[4][c0 + j]);
+            y.y = bn_apply((double)(kv - 2 * (int)acc[j + 1]), bnp[0][c0 + j + 1], bnp[1][c0 + j + 1],
+                           bnp[2][c0 + j + 1], bnp[3][c0 + j + 1], bnp[4][c0 + j + 1]);
+            *reinterpret_cast<double2*>(st + rr0 * 66 + h * kCW + j) = y;
+          }
+        } else {
+          int32_t* st = reinterpret_cast<int32_t*>(smem);
+          // raw = popc(a ^ b) = (K - v) / 2
+          const int m2 = p.raw ? 1 : -2, c2 = p.raw ? (p.K - kv) / 2 : kv;
+#pragma unroll
+          for (int j = 0; j < kCW; j += 4)
+            *reinterpret_cast<int4*>(st + rr0 * 68 + h * kCW + j) =
+                make_int4(c2 + m2 * (int)acc[j], c2 + m2 * (int)acc[j + 1], c2 + m2 * (int)acc[j + 2],
+                          c2 + m2 * (int)acc[j + 3]);
         }
-        __syncthreads();
-        const int nb = n0 + hb * 64;
+      }
+      __syncthreads();
+      const int nb = n0 + hb * 64;
+      if (warp < kEW && p.mode == EPI_F64) {
+        const double* st = reinterpret_cast<const double*>(smem);
         const bool vec = (p.N & 1) == 0 && nb + 64 <= p.N;
-        for (int rr = warp; rr < 128; rr += kThreads / 32) {
+        for (int rr = warp; rr < 128; rr += kEW) {
           const int orow = m0 + rr;
           if (orow >= p.M) break;
           const int cc = lane * 2;
           double* dst = p.rout + (size_t)orow * p.N + nb + cc;
-          const double2 v = *reinterpret_cast<const double2*>(st + rr * kPitch + cc);
+          const double2 v = *reinterpret_cast<const double2*>(st + rr * 66 + cc);
           if (vec) {
             *reinterpret_cast<double2*>(dst) = v;
           } else {
@@ -587,29 +653,15 @@ __global__ void __launch_bounds__(bmmp::Smem<BN>::kThreads, BN == 256 ? 1 : 2)
             if (nb + cc + 1 < p.N) dst[1] = v.y;
           }
         }
-      } else {
-        constexpr int kPitch = 68;
-        int32_t* st = reinterpret_cast<int32_t*>(smem);
-        // raw = popc(a ^ b) = (K - v) / 2
-        const int m2 = p.raw ? 1 : -2, c2 = p.raw ? (p.K - kv) / 2 : kv;
-#pragma unroll
-        for (int j = 0; j < kCW; j += 4) {
-          int4 v;
-          v.x = c2 + m2 * (int)acc[j];
-          v.y = c2 + m2 * (int)acc[j + 1];
-          v.z = c2 + m2 * (int)acc[j + 2];
-          v.w = c2 + m2 * (int)acc[j + 3];
-          *reinterpret_cast<int4*>(st + rr0 * kPitch + h * kCW + j) = v;
-        }
-        __syncthreads();
-        const int nb = n0 + hb * 64;
+      } else if (warp < kEW) {
+        const int32_t* st = reinterpret_cast<const int32_t*>(smem);
         const bool vec = (p.N & 3) == 0 && nb + 64 <= p.N;
-        for (int rr = warp * 2 + (lane >> 4); rr < 128; rr += 2 * (kThreads / 32)) {
+        for (int rr = warp * 2 + (lane >> 4); rr < 128; rr += 2 * kEW) {
           const int orow = m0 + rr;
           if (orow >= p.M) break;
           const int cc = (lane & 15) * 4;
           int32_t* dst = p.out + (size_t)orow * p.N + nb + cc;
-          const int4 v = *reinterpret_cast<const int4*>(st + rr * kPitch + cc);
+          const int4 v = *reinterpret_cast<const int4*>(st + rr * 68 + cc);
           if (vec) {
             *reinterpret_cast<int4*>(dst) = v;
           } else {
@@ -660,11 +712,11 @@ static void launch_bmm_pipe_bn(const BmmTcArgs& p, cudaStream_t st) {
   BT_CUDA(cudaGetDevice(&dev));
   if (configured != dev) {
     BT_CUDA(cudaFuncSetAttribute(bmm_pipe_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 bmmp::Smem<BN>::kBytes));
+                                 bmmp::Cfg<BN>::kBytes));
     configured = dev;
   }
   const dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + 127) / 128));
-  bmm_pipe_kernel<BN><<<grid, bmmp::Smem<BN>::kThreads, bmmp::Smem<BN>::kBytes, st>>>(p);
+  bmm_pipe_kernel<BN><<<grid, bmmp::Cfg<BN>::kThreads, bmmp::Cfg<BN>::kBytes, st>>>(p);
   BT_CUDA(cudaGetLastError());
   note_tc_launch(p.mode == EPI_BITS ? "bmm_pipe/bin" : p.mode == EPI_F64 ? "bmm_pipe/bn" : "bmm_pipe/i32",
                  (int)(grid.x * grid.y), (int)(grid.x * grid.y));
