@@ -384,17 +384,21 @@ constexpr int kPD = 4;         // packed-bit prefetch distance in K-steps
 constexpr int kPS = kPD + 1;   // packed staging slots per thread
 template <int BN>
 struct Cfg {
-  static constexpr int kAW = BN == 256 ? 8 : 4;            // A warps
-  static constexpr int kBW = BN == 256 ? 8 : 4;            // B warps
-  static constexpr int kEW = kAW + kBW;                    // epilogue warps (all producers)
-  static constexpr int kHG = kEW / 4;                      // epilogue warps per lane quarter
-  static constexpr int kThreads = 32 * (kEW + 1);          // + the MMA warp
-  static constexpr int kAWords = 4 * 4 / kAW;              // A words per thread per K-step
-  static constexpr int kBWords = 4 * BN / (32 * kBW);      // B words per thread per K-step
+  // producer warps form kSG step groups (group g takes K-steps g, g + kSG, ...), so a warp's
+  // serial per-step chain (stage -> expand -> store -> arrive) may take kSG MMA steps
+  static constexpr int kSG = BN == 256 ? 2 : 1;
+  static constexpr int kAW = 4 * kSG;                          // A warps (a row's 4 words each)
+  static constexpr int kBWG = BN / 32 > 4 ? BN / 32 : 4;       // B warps per step group
+  static constexpr int kBW = kBWG * kSG;                       // B warps
+  static constexpr int kPW = kAW + kBW;                        // producer warps
+  static constexpr int kEW = BN == 256 ? 16 : 8;               // epilogue warps (the first ones)
+  static constexpr int kHG = kEW / 4;                          // epilogue warps per lane quarter
+  static constexpr int kThreads = 32 * (kPW + 1);              // + the MMA warp
+  static constexpr int kBWords = 4 * BN / (32 * kBWG);         // B words per thread per K-step
   static constexpr int kTmemCols = BN == 256 ? 512 : 256;  // BN accumulator + kR x 32 A columns
   static constexpr int kBSlot = BN * 128;                  // expanded B of one K-step
   static constexpr int kOffStage = kR * kBSlot;            // per-thread packed staging
-  static constexpr int kMain = kOffStage + kPS * 32 * kEW * 16;
+  static constexpr int kMain = kOffStage + kPS * 32 * kPW * 16;
   static constexpr int kEpi = 128 * 68 * 8;                // epilogue staging: 128 x 64 columns
   static constexpr int kMax = kMain > kEpi ? kMain : kEpi;
   // >= 80 KB: at most two CTAs per SM, so their TMEM allocations always fit
@@ -413,7 +417,7 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
   __shared__ uint32_t tmem_base_sh;
   __shared__ int2 thr[BN];
   __shared__ double bnp[5][BN];
-  __shared__ int pa_sh[L::kAW / 4][128];  // per A row: set bits below K, per word share
+  __shared__ int pa_sh[L::kSG][128];  // per A row: set bits below K, per step group
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m0 = blockIdx.y * 128, n0 = blockIdx.x * BN;
   const int KS = p.Kp / 128;  // K-steps = 16-byte chunks per packed row
@@ -422,8 +426,8 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
   const uint8_t* gb = reinterpret_cast<const uint8_t*>(p.b);
   if (tid == 0) {
     for (int r = 0; r < kR; ++r) {
-      mbar_init(&full_a[r], L::kAW);
-      mbar_init(&full_b[r], L::kBW);
+      mbar_init(&full_a[r], 4);
+      mbar_init(&full_b[r], L::kBWG);
       mbar_init(&empty[r], 1);
     }
     mbar_init(&acc_done, 1);
@@ -456,79 +460,71 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
   const uint32_t tbase = tmem_base_sh;
   int pa = 0;
   auto valid = [](int r_) { return r_ >= 32 ? ~0u : r_ > 0 ? (1u << r_) - 1u : 0u; };
+  constexpr int SG = L::kSG;
   if (warp < L::kAW) {
-    // ================= A producers: row q*32 + lane, words ag*kAWords .. of each K-step =================
-    const int q = warp & 3, ag = warp >> 2, row = q * 32 + lane;
-    constexpr int NWd = L::kAWords;
+    // ================= A producers: row q*32 + lane, the K-steps of step group g =================
+    const int q = warp & 3, g = warp >> 2, row = q * 32 + lane;
     const bool ok = m0 + row < p.M;
-    const uint8_t* src = ga + (size_t)(ok ? m0 + row : 0) * KS * 16 + ag * NWd * 4;
+    const uint8_t* src = ga + (size_t)(ok ? m0 + row : 0) * KS * 16;
     uint8_t* stg = smem + L::kOffStage + (size_t)tid * kPS * 16;
-    auto issue = [&](int s) {
-      if (s < KS) {
-        if constexpr (NWd == 4) cp_async16(smem_u32(stg + (s % kPS) * 16), src + (size_t)s * 16, ok ? 16 : 0);
-        else asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stg + (s % kPS) * 16)),
-                          "l"(src + (size_t)s * 16), "r"(ok ? 8 : 0) : "memory");
-      }
+    auto issue = [&](int i) {  // this thread's i-th K-step, s = g + i*SG
+      const int s = g + i * SG;
+      if (s < KS) cp_async16(smem_u32(stg + (i % kPS) * 16), src + (size_t)s * 16, ok ? 16 : 0);
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll
-    for (int s = 0; s < kPD; ++s) issue(s);
-    for (int s = 0; s < KS; ++s) {
-      issue(s + kPD);
+    for (int i = 0; i < kPD; ++i) issue(i);
+    for (int i = 0, s = g; s < KS; ++i, s += SG) {
+      issue(i + kPD);
       asm volatile("cp.async.wait_group %0;" ::"n"(kPD) : "memory");
       const int r = s % kR;
-      uint32_t w[NWd], v[8 * NWd];
-      if constexpr (NWd == 4) {
-        const uint4 b4 = *reinterpret_cast<const uint4*>(stg + (s % kPS) * 16);
-        w[0] = b4.x; w[1] = b4.y; w[2] = b4.z; w[3] = b4.w;
-      } else {
-        const uint2 b2 = *reinterpret_cast<const uint2*>(stg + (s % kPS) * 16);
-        w[0] = b2.x; w[1] = b2.y;
-      }
-      const int rem = p.K - 32 * (4 * s + ag * NWd);
+      uint32_t v[32];
+      const uint4 b4 = *reinterpret_cast<const uint4*>(stg + (i % kPS) * 16);
+      const uint32_t w[4] = {b4.x, b4.y, b4.z, b4.w};
+      const int rem = p.K - 128 * s;
 #pragma unroll
-      for (int i = 0; i < NWd; ++i) {
-        expand_word(w[i], v + 8 * i);
-        pa += __popc(w[i] & valid(rem - 32 * i));
+      for (int k = 0; k < 4; ++k) {
+        expand_word(w[k], v + 8 * k);
+        pa += __popc(w[k] & valid(rem - 32 * k));
       }
       if (s >= kR) mbar_wait(&empty[r], (uint32_t)((s / kR - 1) & 1));  // MMAs of step s - kR done
-      const uint32_t ta = taddr(tbase, q * 32, (uint32_t)(BN + r * 32 + 8 * ag * NWd));
-      if constexpr (NWd == 4) tmem_st32(ta, v);
-      else tmem_st16(ta, v);
+      tmem_st32(taddr(tbase, q * 32, (uint32_t)(BN + r * 32)), v);
       tmem_st_wait();
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_a[r]);
     }
-    pa_sh[ag][row] = pa;
-  } else if (warp < L::kEW) {
-    // ================= B producers: column n, words bg*kBWords .. of each K-step =================
+    pa_sh[g][row] = pa;
+  } else if (warp < L::kPW) {
+    // ================= B producers: column n, words bg*kBWords .. of the K-steps of group g =================
     const int bt = tid - 32 * L::kAW;  // 0 .. 32*kBW - 1
+    const int g = bt / (32 * L::kBWG), gt = bt % (32 * L::kBWG);
     constexpr int NWd = L::kBWords;
-    const int n = bt % BN, bg = bt / BN;
+    const int n = gt % BN, bg = gt / BN;
     const bool ok = n0 + n < p.N;
     const uint8_t* src = gb + (size_t)(ok ? n0 + n : 0) * KS * 16 + bg * NWd * 4;
     uint8_t* stg = smem + L::kOffStage + (size_t)tid * kPS * 16;
-    auto issue = [&](int s) {
+    auto issue = [&](int i) {
+      const int s = g + i * SG;
       if (s < KS) {
-        if constexpr (NWd == 4) cp_async16(smem_u32(stg + (s % kPS) * 16), src + (size_t)s * 16, ok ? 16 : 0);
-        else asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stg + (s % kPS) * 16)),
+        if constexpr (NWd == 4) cp_async16(smem_u32(stg + (i % kPS) * 16), src + (size_t)s * 16, ok ? 16 : 0);
+        else asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(stg + (i % kPS) * 16)),
                           "l"(src + (size_t)s * 16), "r"(ok ? 8 : 0) : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
 #pragma unroll
-    for (int s = 0; s < kPD; ++s) issue(s);
-    for (int s = 0; s < KS; ++s) {
-      issue(s + kPD);
+    for (int i = 0; i < kPD; ++i) issue(i);
+    for (int i = 0, s = g; s < KS; ++i, s += SG) {
+      issue(i + kPD);
       asm volatile("cp.async.wait_group %0;" ::"n"(kPD) : "memory");
       const int r = s % kR;
       uint32_t w[NWd];
       if constexpr (NWd == 4) {
-        const uint4 b4 = *reinterpret_cast<const uint4*>(stg + (s % kPS) * 16);
+        const uint4 b4 = *reinterpret_cast<const uint4*>(stg + (i % kPS) * 16);
         w[0] = b4.x; w[1] = b4.y; w[2] = b4.z; w[3] = b4.w;
       } else {
-        const uint2 b2 = *reinterpret_cast<const uint2*>(stg + (s % kPS) * 16);
+        const uint2 b2 = *reinterpret_cast<const uint2*>(stg + (i % kPS) * 16);
         w[0] = b2.x; w[1] = b2.y;
       }
       const int rem = p.K - 32 * (4 * s + bg * NWd);
@@ -573,7 +569,7 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
     const int rr0 = q * 32 + lane, row = m0 + rr0;
     int kv = p.K;
 #pragma unroll
-    for (int j = 0; j < L::kAW / 4; ++j) kv -= 2 * pa_sh[j][rr0];
+    for (int j = 0; j < SG; ++j) kv -= 2 * pa_sh[j][rr0];
     if (p.mode == EPI_BITS) {
 #pragma unroll 1
       for (int c0 = h * (BN / kHG); c0 < (h + 1) * (BN / kHG); c0 += 16) {
@@ -603,7 +599,7 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
     int kv = p.K;
     if (warp < kEW) {
 #pragma unroll
-      for (int j = 0; j < L::kAW / 4; ++j) kv -= 2 * pa_sh[j][rr0];
+      for (int j = 0; j < SG; ++j) kv -= 2 * pa_sh[j][rr0];
     }
 #pragma unroll 1
     for (int hb = 0; hb < BN / 64; ++hb) {
