@@ -49,6 +49,7 @@ struct BmmTcArgs {
   int cwo32;               // output words (32-bit) per row
   const long long* thr_lo;  // EPI_BITS: per column lo / hi (nullptr: v >= 0)
   const long long* thr_hi;
+  const uint8_t* bpre;  // pipelined kernel, PRE: B expanded to {0,1} blocks (bmm_expand_b01_kernel)
 };
 
 // Staging slot of 16-byte chunk c of packed row r (cpr chunks per row): c ^ (r & 7) when that
@@ -382,23 +383,24 @@ namespace bmmp {
 constexpr int kR = 4;          // ring depth: expanded B slots (smem) and A slots (TMEM)
 constexpr int kPD = 4;         // packed-bit prefetch distance in K-steps
 constexpr int kPS = kPD + 1;   // packed staging slots per thread
-template <int BN>
+template <int BN, bool PRE>
 struct Cfg {
   // producer warps form kSG step groups (group g takes K-steps g, g + kSG, ...), so a warp's
   // serial per-step chain (stage -> expand -> store -> arrive) may take kSG MMA steps
   static constexpr int kSG = BN == 256 ? 2 : 1;
   static constexpr int kAW = 4 * kSG;                          // A warps (a row's 4 words each)
-  static constexpr int kBWG = BN / 32 > 4 ? BN / 32 : 4;       // B warps per step group
+  // B warps per step group (PRE: none; one loader warp copies the pre-expanded blocks)
+  static constexpr int kBWG = PRE ? 0 : BN / 32 > 4 ? BN / 32 : 4;
   static constexpr int kBW = kBWG * kSG;                       // B warps
-  static constexpr int kPW = kAW + kBW;                        // producer warps
-  static constexpr int kEW = BN == 256 ? 16 : 8;               // epilogue warps (the first ones)
+  static constexpr int kPW = kAW + kBW + (PRE ? 1 : 0);        // producer warps
+  static constexpr int kEW = PRE ? kAW : BN == 256 ? 16 : 8;   // epilogue warps (the first ones)
   static constexpr int kHG = kEW / 4;                          // epilogue warps per lane quarter
   static constexpr int kThreads = 32 * (kPW + 1);              // + the MMA warp
-  static constexpr int kBWords = 4 * BN / (32 * kBWG);         // B words per thread per K-step
+  static constexpr int kBWords = PRE ? 4 : 4 * BN / (32 * kBWG);  // B words per thread per K-step
   static constexpr int kTmemCols = BN == 256 ? 512 : 256;  // BN accumulator + kR x 32 A columns
   static constexpr int kBSlot = BN * 128;                  // expanded B of one K-step
   static constexpr int kOffStage = kR * kBSlot;            // per-thread packed staging
-  static constexpr int kMain = kOffStage + kPS * 32 * kPW * 16;
+  static constexpr int kMain = kOffStage + kPS * 32 * (kAW + kBW) * 16;
   static constexpr int kEpi = 128 * 68 * 8;                // epilogue staging: 128 x 64 columns
   static constexpr int kMax = kMain > kEpi ? kMain : kEpi;
   // >= 80 KB: at most two CTAs per SM, so their TMEM allocations always fit
@@ -406,11 +408,11 @@ struct Cfg {
 };
 }  // namespace bmmp
 
-template <int BN>
-__global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
+template <int BN, bool PRE>
+__global__ void __launch_bounds__(bmmp::Cfg<BN, PRE>::kThreads, BN == 256 ? 1 : 2)
     bmm_pipe_kernel(const __grid_constant__ BmmTcArgs p) {
   using namespace umma;
-  using L = bmmp::Cfg<BN>;
+  using L = bmmp::Cfg<BN, PRE>;
   constexpr int kThreads = L::kThreads, kHG = L::kHG, kR = bmmp::kR, kPD = bmmp::kPD, kPS = bmmp::kPS;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full_a[kR], full_b[kR], empty[kR], acc_done;
@@ -427,7 +429,7 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
   if (tid == 0) {
     for (int r = 0; r < kR; ++r) {
       mbar_init(&full_a[r], 4);
-      mbar_init(&full_b[r], L::kBWG);
+      mbar_init(&full_b[r], PRE ? 1 : L::kBWG);
       mbar_init(&empty[r], 1);
     }
     mbar_init(&acc_done, 1);
@@ -495,7 +497,19 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN>::kThreads, BN == 256 ? 1 : 2)
       if (lane == 0) mbar_arrive(&full_a[r]);
     }
     pa_sh[g][row] = pa;
-  } else if (warp < L::kPW) {
+  } else if (PRE && warp == L::kAW) {
+    // ================= B loader: one bulk copy per K-step of the pre-expanded block =================
+    if (lane == 0) {
+      const uint8_t* src = p.bpre + (size_t)blockIdx.x * KS * L::kBSlot;
+      for (int s = 0; s < KS; ++s) {
+        const int r = s % kR;
+        if (s >= kR) mbar_wait(&empty[r], (uint32_t)((s / kR - 1) & 1));
+        mbar_arrive_expect_tx(&full_b[r], (uint32_t)L::kBSlot);
+        for (int off = 0; off < L::kBSlot; off += 16384)
+          bulk_g2s(bring + (size_t)r * L::kBSlot + off, src + (size_t)s * L::kBSlot + off, 16384u, &full_b[r]);
+      }
+    }
+  } else if (!PRE && warp < L::kPW) {
     // ================= B producers: column n, words bg*kBWords .. of the K-steps of group g =================
     const int bt = tid - 32 * L::kAW;  // 0 .. 32*kBW - 1
     const int g = bt / (32 * L::kBWG), gt = bt % (32 * L::kBWG);
@@ -701,34 +715,79 @@ static BmmTcArgs bmm_args(int M, int N, int K, const uint64_t* a, const uint64_t
   return p;
 }
 
-template <int BN>
+// B (ColPacked N x Kp bits) -> {0,1} byte blocks for the PRE kernel: block (N-tile t, K-step s)
+// of BN columns x 128 bytes in the canonical K-major layout the MMA reads, bits past K and
+// columns past N zero. One thread per (column, K-step, 32-bit word).
+__global__ void bmm_expand_b01_kernel(const uint32_t* __restrict__ b, int N, int K, int KS, int BN, int npad,
+                                      uint8_t* __restrict__ out) {
+  const long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= (long long)npad * KS * 4) return;
+  const int n = (int)(item % npad);
+  const long long rest = item / npad;
+  const int u = (int)(rest & 3), s = (int)(rest >> 2);
+  const int i = 4 * s + u, rem = K - 32 * i;
+  uint32_t w = n < N && rem > 0 ? __ldg(b + (size_t)n * KS * 4 + i) : 0u;
+  if (rem < 32) w &= rem > 0 ? (1u << rem) - 1u : 0u;
+  uint32_t o[8];
+  expand_word01(w, o);
+  const int t = n / BN, nn = n % BN;
+  uint8_t* dst = out + ((size_t)t * KS + s) * BN * 128 + (nn >> 3) * 1024 + (2 * u) * 128 + (nn & 7) * 16;
+  *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
+  *reinterpret_cast<uint4*>(dst + 128) = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+template <int BN, bool PRE>
 static void launch_bmm_pipe_bn(const BmmTcArgs& p, cudaStream_t st) {
+  using L = bmmp::Cfg<BN, PRE>;
   static thread_local int configured = -1;
   int dev = 0;
   BT_CUDA(cudaGetDevice(&dev));
   if (configured != dev) {
-    BT_CUDA(cudaFuncSetAttribute(bmm_pipe_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 bmmp::Cfg<BN>::kBytes));
+    BT_CUDA(cudaFuncSetAttribute(bmm_pipe_kernel<BN, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes));
     configured = dev;
   }
   const dim3 grid((unsigned)((p.N + BN - 1) / BN), (unsigned)((p.M + 127) / 128));
-  bmm_pipe_kernel<BN><<<grid, bmmp::Cfg<BN>::kThreads, bmmp::Cfg<BN>::kBytes, st>>>(p);
+  bmm_pipe_kernel<BN, PRE><<<grid, L::kThreads, L::kBytes, st>>>(p);
   BT_CUDA(cudaGetLastError());
   note_tc_launch(p.mode == EPI_BITS ? "bmm_pipe/bin" : p.mode == EPI_F64 ? "bmm_pipe/bn" : "bmm_pipe/i32",
                  (int)(grid.x * grid.y), (int)(grid.x * grid.y));
 }
 
-// Any M, N, K: 128 x 256 tiles (one CTA per SM, N = 256 MMAs) when they fill every SM at least
-// twice, else 128 x 128 tiles when they fill the two CTA slots per SM, else 128 x 64.
+// per host thread and device: the pre-expanded B workspace of the last call
+struct BpreWs {
+  int dev = -1;
+  DevBuf buf;
+};
+static thread_local BpreWs g_bpre;
+
+// Any M, N, K: 128 x 256 tiles (one CTA per SM, N = 256 MMAs; B expanded once per call into a
+// workspace by bmm_expand_b01_kernel and streamed by bulk copies) when they fill every SM at
+// least twice, else 128 x 128 tiles when they fill the two CTA slots per SM, else 128 x 64
+// (B expanded in the GEMM by its own producer warps).
 void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
-  const BmmTcArgs p = bmm_args(M, N, K, a, b, e);
+  BmmTcArgs p = bmm_args(M, N, K, a, b, e);
   int dev = 0, sms = 148;
   BT_CUDA(cudaGetDevice(&dev));
   BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const long long mt = (M + 127) / 128;
-  if (mt * ((N + 255) / 256) >= 2LL * sms) launch_bmm_pipe_bn<256>(p, st);
-  else if (mt * ((N + 127) / 128) >= 2LL * sms) launch_bmm_pipe_bn<128>(p, st);
-  else launch_bmm_pipe_bn<64>(p, st);
+  if (mt * ((N + 255) / 256) >= 2LL * sms) {
+    const int KS = p.Kp / 128, npad = (N + 255) / 256 * 256;
+    const size_t bytes = (size_t)npad * KS * 128;
+    if (g_bpre.dev != dev || g_bpre.buf.bytes() < bytes) {
+      g_bpre.buf.alloc(bytes);
+      g_bpre.dev = dev;
+    }
+    const long long items = (long long)npad * KS * 4;
+    bmm_expand_b01_kernel<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const uint32_t*>(b), N, K, KS, 256, npad, g_bpre.buf.get<uint8_t>());
+    BT_CUDA(cudaGetLastError());
+    p.bpre = g_bpre.buf.get<uint8_t>();
+    launch_bmm_pipe_bn<256, true>(p, st);
+  } else if (mt * ((N + 127) / 128) >= 2LL * sms) {
+    launch_bmm_pipe_bn<128, false>(p, st);
+  } else {
+    launch_bmm_pipe_bn<64, false>(p, st);
+  }
 }
 
 static std::atomic<int> g_bmm_kernel{BTNN_BMM_AUTO};

@@ -113,7 +113,7 @@ def test_bmm_random_sweep_pipelined(pipelined):
 
 
 @pytest.mark.parametrize("m,n,k", [(300, 700, 1536), (129, 1, 33), (1, 129, 1408), (130, 131, 1537), (257, 300, 4160),
-                                   (1024, 1100, 9216), (512, 512, 25088), (96, 2000, 4097), (8192, 1200, 300)])
+                                   (1024, 1100, 9216), (512, 512, 25088), (96, 2000, 4097), (8192, 1200, 300), (8192, 2304, 1100)])
 def test_bmm_pipelined_shapes(m, n, k, pipelined, engine):
     """K-pipelined packed BMM: tile edges in M and N (128 x 64 and 128 x 128 tiles), K-step
     counts below and above the ring and prefetch depths, partial last words; pm1, raw and
