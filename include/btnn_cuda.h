@@ -112,8 +112,9 @@ enum { BTNN_ENGINE_AUTO = 0, BTNN_ENGINE_POPC = 1, BTNN_ENGINE_TC = 2 };
 int btnn_cuda_set_engine(int engine);
 /* Packed-operand BMM kernel for bmm_pm1 / bmm_raw / bmm_pm1_bin and fully-connected plan layers
  * (process-wide): 0 = auto (whole-K on-chip kernel when K <= 1536, else K-pipelined),
- * 1 = whole-K (fails with BTNN_UNSUPPORTED_SHAPE when K > 1536), 2 = K-pipelined. */
-enum { BTNN_BMM_AUTO = 0, BTNN_BMM_WHOLE_K = 1, BTNN_BMM_PIPELINED = 2 };
+ * 1 = whole-K (fails with BTNN_UNSUPPORTED_SHAPE when K > 1536), 2 = K-pipelined, 3 = K-pipelined
+ * with B always expanded inside the GEMM (the variant plan layers use; for tests). */
+enum { BTNN_BMM_AUTO = 0, BTNN_BMM_WHOLE_K = 1, BTNN_BMM_PIPELINED = 2, BTNN_BMM_PIPELINED_NO_PRE = 3 };
 int btnn_cuda_set_bmm_kernel(int which);
 
 /* ---- storage sizes (words of uint64) --------------------------------------------- */

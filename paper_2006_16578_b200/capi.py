@@ -187,9 +187,10 @@ def set_engine(engine: int) -> None:
     check(lib().btnn_cuda_set_engine(engine))
 
 
-BMM_AUTO, BMM_WHOLE_K, BMM_PIPELINED = range(3)
+BMM_AUTO, BMM_WHOLE_K, BMM_PIPELINED, BMM_PIPELINED_NO_PRE = range(4)
 
 
 def set_bmm_kernel(which: int) -> None:
-    """btnn_cuda_set_bmm_kernel: 0 auto, 1 whole-K on-chip kernel (K <= 1536), 2 K-pipelined."""
+    """btnn_cuda_set_bmm_kernel: 0 auto, 1 whole-K on-chip kernel (K <= 1536), 2 K-pipelined,
+    3 K-pipelined with B expanded inside the GEMM."""
     check(lib().btnn_cuda_set_bmm_kernel(which))

@@ -94,7 +94,8 @@ bool bmm_tc_supported(int M, int N, int K);
 void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st);
 // K-pipelined packed BMM for any inner dimension (bmm_tc.cu, bmm_pipe_kernel): same operands
 // and epilogues as launch_bmm_tc.
-void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st);
+void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st,
+                     bool pre_b);
 // Either of the two per btnn_cuda_set_bmm_kernel (auto: whole-K when it fits); returns the
 // engine name ("tc_i8_bmm" / "tc_i8_bmm_pipe").
 const char* launch_bmm_packed(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e,

@@ -505,8 +505,10 @@ __global__ void __launch_bounds__(bmmp::Cfg<BN, PRE>::kThreads, BN == 256 ? 1 : 
         const int r = s % kR;
         if (s >= kR) mbar_wait(&empty[r], (uint32_t)((s / kR - 1) & 1));
         mbar_arrive_expect_tx(&full_b[r], (uint32_t)L::kBSlot);
-        for (int off = 0; off < L::kBSlot; off += 16384)
-          bulk_g2s(bring + (size_t)r * L::kBSlot + off, src + (size_t)s * L::kBSlot + off, 16384u, &full_b[r]);
+        constexpr int kChunk = L::kBSlot < 16384 ? L::kBSlot : 16384;
+#pragma unroll
+        for (int off = 0; off < L::kBSlot; off += kChunk)
+          bulk_g2s(bring + (size_t)r * L::kBSlot + off, src + (size_t)s * L::kBSlot + off, (uint32_t)kChunk, &full_b[r]);
       }
     }
   } else if (!PRE && warp < L::kPW) {
@@ -760,17 +762,23 @@ struct BpreWs {
 };
 static thread_local BpreWs g_bpre;
 
-// Any M, N, K: 128 x 256 tiles (one CTA per SM, N = 256 MMAs; B expanded once per call into a
-// workspace by bmm_expand_b01_kernel and streamed by bulk copies) when they fill every SM at
-// least twice, else 128 x 128 tiles when they fill the two CTA slots per SM, else 128 x 64
-// (B expanded in the GEMM by its own producer warps).
-void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
+// Any M, N, K. 128 x 256 tiles (one CTA per SM, N = 256 MMAs) when they occupy at least half
+// the SMs: with pre_b (kernel-level calls, which own the workspace for the duration of the call)
+// B is expanded once into {0,1} blocks by bmm_expand_b01_kernel and streamed by bulk copies,
+// else expanded in the GEMM by its own producer warps. Otherwise 128 x 128 tiles when they fill
+// the two CTA slots per SM, else 128 x 64.
+void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st,
+                     bool pre_b) {
   BmmTcArgs p = bmm_args(M, N, K, a, b, e);
   int dev = 0, sms = 148;
   BT_CUDA(cudaGetDevice(&dev));
   BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const long long mt = (M + 127) / 128;
-  if (mt * ((N + 255) / 256) >= 2LL * sms) {
+  if (2 * mt * ((N + 255) / 256) >= sms) {
+    if (!pre_b) {
+      launch_bmm_pipe_bn<256, false>(p, st);
+      return;
+    }
     const int KS = p.Kp / 128, npad = (N + 255) / 256 * 256;
     const size_t bytes = (size_t)npad * KS * 128;
     if (g_bpre.dev != dev || g_bpre.buf.bytes() < bytes) {
@@ -803,7 +811,7 @@ const char* launch_bmm_packed(int M, int N, int K, const uint64_t* a, const uint
     launch_bmm_tc(M, N, K, a, b, e, st);
     return "tc_i8_bmm";
   }
-  launch_bmm_pipe(M, N, K, a, b, e, st);
+  launch_bmm_pipe(M, N, K, a, b, e, st, k != BTNN_BMM_PIPELINED_NO_PRE);
   return "tc_i8_bmm_pipe";
 }
 
@@ -812,7 +820,7 @@ const char* launch_bmm_packed(int M, int N, int K, const uint64_t* a, const uint
 // split-K implicit GEMM (few output tiles, long K).
 const char* launch_bmm_fc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
   const int k = g_bmm_kernel.load();
-  if (k != BTNN_BMM_PIPELINED && bmm_tc_supported(M, N, K)) {
+  if (k < BTNN_BMM_PIPELINED && bmm_tc_supported(M, N, K)) {
     launch_bmm_tc(M, N, K, a, b, e, st);
     return "tc_i8_bmm";
   }
@@ -820,8 +828,8 @@ const char* launch_bmm_fc(int M, int N, int K, const uint64_t* a, const uint64_t
   BT_CUDA(cudaGetDevice(&dev));
   BT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const long long tiles = (long long)((M + 127) / 128) * ((N + 63) / 64);
-  if (k == BTNN_BMM_PIPELINED || (k == BTNN_BMM_AUTO && tiles >= sms)) {
-    launch_bmm_pipe(M, N, K, a, b, e, st);
+  if (k >= BTNN_BMM_PIPELINED || (k == BTNN_BMM_AUTO && tiles >= sms)) {
+    launch_bmm_pipe(M, N, K, a, b, e, st, false);  // (captured into plan graphs: no shared workspace)
     return "tc_i8_bmm_pipe";
   }
   return nullptr;
@@ -831,7 +839,7 @@ const char* launch_bmm_fc(int M, int N, int K, const uint64_t* a, const uint64_t
 
 extern "C" int btnn_cuda_set_bmm_kernel(int which) {
   return btnn_gpu::guard([&] {
-    btnn_gpu::require(which >= BTNN_BMM_AUTO && which <= BTNN_BMM_PIPELINED, BTNN_INVALID_INPUT,
+    btnn_gpu::require(which >= BTNN_BMM_AUTO && which <= BTNN_BMM_PIPELINED_NO_PRE, BTNN_INVALID_INPUT,
                       "set_bmm_kernel: unknown kernel");
     btnn_gpu::g_bmm_kernel.store(which);
   });

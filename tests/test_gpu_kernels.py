@@ -93,9 +93,10 @@ def test_bmm_packed_kernel_shapes(m, n, k, engine):
     assert np.array_equal(np.asarray(bits).reshape(-1), words.reshape(-1))
 
 
-@pytest.fixture
-def pipelined():
-    capi.set_bmm_kernel(capi.BMM_PIPELINED)
+@pytest.fixture(params=["pre", "in-kernel"])
+def pipelined(request):
+    """The K-pipelined packed BMM, with B pre-expanded for 128 x 256 tiles or always in-kernel."""
+    capi.set_bmm_kernel(capi.BMM_PIPELINED if request.param == "pre" else capi.BMM_PIPELINED_NO_PRE)
     yield
     capi.set_bmm_kernel(capi.BMM_AUTO)
 
