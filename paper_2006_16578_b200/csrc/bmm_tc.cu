@@ -719,23 +719,26 @@ static BmmTcArgs bmm_args(int M, int N, int K, const uint64_t* a, const uint64_t
 
 // B (ColPacked N x Kp bits) -> {0,1} byte blocks for the PRE kernel: block (N-tile t, K-step s)
 // of BN columns x 128 bytes in the canonical K-major layout the MMA reads, bits past K and
-// columns past N zero. One thread per (column, K-step, 32-bit word).
-__global__ void bmm_expand_b01_kernel(const uint32_t* __restrict__ b, int N, int K, int KS, int BN, int npad,
+// columns past N zero. One thread per (column, K-step): one 16-byte load, eight 16-byte stores
+// (consecutive threads on consecutive columns: 128 contiguous bytes per 8 lanes).
+__global__ void bmm_expand_b01_kernel(const uint4* __restrict__ b, int N, int K, int KS, int BN, int npad,
                                       uint8_t* __restrict__ out) {
   const long long item = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (item >= (long long)npad * KS * 4) return;
-  const int n = (int)(item % npad);
-  const long long rest = item / npad;
-  const int u = (int)(rest & 3), s = (int)(rest >> 2);
-  const int i = 4 * s + u, rem = K - 32 * i;
-  uint32_t w = n < N && rem > 0 ? __ldg(b + (size_t)n * KS * 4 + i) : 0u;
-  if (rem < 32) w &= rem > 0 ? (1u << rem) - 1u : 0u;
-  uint32_t o[8];
-  expand_word01(w, o);
+  if (item >= (long long)npad * KS) return;
+  const int n = (int)(item % npad), s = (int)(item / npad);
+  const uint4 b4 = n < N ? __ldg(b + (size_t)n * KS + s) : make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t w4[4] = {b4.x, b4.y, b4.z, b4.w};
   const int t = n / BN, nn = n % BN;
-  uint8_t* dst = out + ((size_t)t * KS + s) * BN * 128 + (nn >> 3) * 1024 + (2 * u) * 128 + (nn & 7) * 16;
-  *reinterpret_cast<uint4*>(dst) = make_uint4(o[0], o[1], o[2], o[3]);
-  *reinterpret_cast<uint4*>(dst + 128) = make_uint4(o[4], o[5], o[6], o[7]);
+  uint8_t* dst = out + ((size_t)t * KS + s) * BN * 128 + (nn >> 3) * 1024 + (nn & 7) * 16;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int rem = K - 32 * (4 * s + u);
+    const uint32_t w = rem >= 32 ? w4[u] : rem > 0 ? w4[u] & ((1u << rem) - 1u) : 0u;
+    uint32_t o[8];
+    expand_word01(w, o);
+    *reinterpret_cast<uint4*>(dst + (2 * u) * 128) = make_uint4(o[0], o[1], o[2], o[3]);
+    *reinterpret_cast<uint4*>(dst + (2 * u + 1) * 128) = make_uint4(o[4], o[5], o[6], o[7]);
+  }
 }
 
 template <int BN, bool PRE>
@@ -785,9 +788,9 @@ void launch_bmm_pipe(int M, int N, int K, const uint64_t* a, const uint64_t* b, 
       g_bpre.buf.alloc(bytes);
       g_bpre.dev = dev;
     }
-    const long long items = (long long)npad * KS * 4;
+    const long long items = (long long)npad * KS;
     bmm_expand_b01_kernel<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(
-        reinterpret_cast<const uint32_t*>(b), N, K, KS, 256, npad, g_bpre.buf.get<uint8_t>());
+        reinterpret_cast<const uint4*>(b), N, K, KS, 256, npad, g_bpre.buf.get<uint8_t>());
     BT_CUDA(cudaGetLastError());
     p.bpre = g_bpre.buf.get<uint8_t>();
     launch_bmm_pipe_bn<256, true>(p, st);
