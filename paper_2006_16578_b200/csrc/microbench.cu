@@ -262,6 +262,54 @@ __global__ void __launch_bounds__(576, 1) tc_halo_pattern_kernel(int iters, long
 }
 
 // tcgen05 i8 throughput: one thread issues iters x 4 MMAs (M128 x N x K32) back to back.
+// The exact first layer's MMA stream (kernels_first_tc.cu, AlexNet 11x11/4 geometry): A from
+// SWIZZLE_NONE digit planes with overlapping windows (LBO 16 B, SBO 128 B), per tile 11 kernel
+// rows x 2 K-steps x 6 digits x (128 / N) channel groups, B weight blocks 64 units apart.
+template <int N>
+__global__ void __launch_bounds__(128, 1) tc_fconv_pattern_kernel(int iters, long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int kPlane = 17 * 1024, kRows = 11, kK = 2;
+  uint8_t* bs = smem + 6 * kPlane;  // weights: kRows * kK * 4 blocks of 32 channels x 32 B
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid / 32;
+  if (warp == 0) tmem_alloc(&tbase, 512);
+  for (int i = tid; i < (6 * kPlane + kRows * kK * 4 * 1024) / 16; i += 128)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x01010101u, 0x01020304u, 0, 0x7f7f7f7fu);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tb = tbase;
+  if (tid == 0) {
+    const uint32_t id = idesc_i8(128, N);
+    const uint64_t a0 = sdesc(smem_u32(smem), 16, 128), b0 = sdesc(smem_u32(bs), 128, 256);
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it)
+      for (int grp = 0; grp < 128 / N; ++grp)
+        for (int r = 0; r < kRows; ++r)
+          for (int kc = 0; kc < kK; ++kc) {
+            const uint32_t rowoff = (uint32_t)((r & 3) * 4 + (r >> 2)) * 1024;
+            const uint64_t bd = b0 + (uint64_t)(((r * kK + kc) * 4 + grp * (N / 32)) * 64);
+            const uint64_t ad = a0 + (uint64_t)((rowoff + kc * 32) >> 4);
+#pragma unroll
+            for (int d = 0; d < 6; ++d)
+              mma_i8_ss(tb + (grp & 1) * 192 * (N / 32 == 1) + d * N, ad + (uint64_t)(d * kPlane / 16), bd, id,
+                        (r | kc) != 0);
+          }
+    mma_commit(&bar);
+    mbar_wait(&bar, 0);
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 0) tmem_dealloc(tb, 512);
+}
+
 template <bool ATMEM, int N>
 __global__ void __launch_bounds__(128, 1) tc_peak_kernel(int iters, long long* cycles) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -496,6 +544,22 @@ int main() {
       printf(", \"%s\": {\"tmacs\": %.1f, \"clk_per_mma\": %.1f, \"ms\": %.3f}", name, macs / ms / 1e9,
              mean / (iters * 18.0), ms);
     };
+    auto tcf = [&](auto kern, int N, const char* name) {
+      const int iters = 64;
+      const size_t smem = 6 * 17 * 1024 + 11 * 2 * 4 * 1024;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const float ms = time_ms([&] { kern<<<sms, 128, smem>>>(iters, d_cyc); });
+      std::vector<long long> cyc(sms);
+      cudaMemcpy(cyc.data(), d_cyc, sms * 8, cudaMemcpyDeviceToHost);
+      double mean = 0;
+      for (auto c : cyc) mean += c;
+      mean /= sms;
+      const double mmas = (double)iters * 11 * 2 * 6 * (128 / N);
+      printf(", \"%s\": {\"clk_per_mma\": %.1f, \"clk_per_tile\": %.0f, \"ms\": %.3f}", name, mean / mmas,
+             mean / iters, ms);
+    };
+    tcf(tc_fconv_pattern_kernel<32>, 32, "tc_i8_first_conv_pattern_n32");
+    tcf(tc_fconv_pattern_kernel<64>, 64, "tc_i8_first_conv_pattern_n64");
     tch(tc_halo_pattern_kernel<64, false>, 64, "tc_i8_halo_pattern_n64");
     tch(tc_halo_pattern_kernel<64, true>, 64, "tc_i8_halo_pattern_n64_align1k");
     tch(tc_halo_pattern_kernel<128, false>, 128, "tc_i8_halo_pattern_n128");
