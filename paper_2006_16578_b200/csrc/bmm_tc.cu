@@ -103,20 +103,25 @@ __global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid
   const int cpr = Kp / 128;  // 16-byte chunks per packed row
   uint8_t* a_stage = smem + (size_t)bmmtc::kBN * Kp;          // 128 rows x Kp/8 bytes
   uint8_t* b_stage = a_stage + (size_t)bmmtc::kBM * (Kp / 8);  // 64 columns x Kp/8 bytes
+  // Programmatic dependent launch: the next kernel of the stream may start its prologue now;
+  // B (weights / the second operand) is staged before waiting for the previous kernel, A (the
+  // previous layer's output) and every global write after.
+  grid_dep_launch();
   {
     const uint8_t* ga = reinterpret_cast<const uint8_t*>(p.a);
     const uint8_t* gb = reinterpret_cast<const uint8_t*>(p.b);
-    for (int g = tid; g < bmmtc::kBM * cpr; g += bmmtc::kThreads) {
-      const int r = g / cpr, c = g - r * cpr, row = m0 + r;
-      const bool ok = row < p.M;
-      cp_async16(smem_u32(a_stage + (size_t)r * (Kp / 8) + (size_t)stage_slot(r, c, cpr) * 16),
-                 ga + ((size_t)(ok ? row : 0) * cpr + c) * 16, ok ? 16 : 0);
-    }
     for (int g = tid; g < bmmtc::kBN * cpr; g += bmmtc::kThreads) {
       const int r = g / cpr, c = g - r * cpr, col = n0 + r;
       const bool ok = col < p.N;
       cp_async16(smem_u32(b_stage + (size_t)r * (Kp / 8) + (size_t)stage_slot(r, c, cpr) * 16),
                  gb + ((size_t)(ok ? col : 0) * cpr + c) * 16, ok ? 16 : 0);
+    }
+    grid_dep_wait();
+    for (int g = tid; g < bmmtc::kBM * cpr; g += bmmtc::kThreads) {
+      const int r = g / cpr, c = g - r * cpr, row = m0 + r;
+      const bool ok = row < p.M;
+      cp_async16(smem_u32(a_stage + (size_t)r * (Kp / 8) + (size_t)stage_slot(r, c, cpr) * 16),
+                 ga + ((size_t)(ok ? row : 0) * cpr + c) * 16, ok ? 16 : 0);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
@@ -355,8 +360,7 @@ void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, co
     configured = dev;
   }
   const dim3 grid((unsigned)((N + bmmtc::kBN - 1) / bmmtc::kBN), (unsigned)((M + bmmtc::kBM - 1) / bmmtc::kBM));
-  bmm_tc_kernel<<<grid, bmmtc::kThreads, smem, st>>>(p);
-  BT_CUDA(cudaGetLastError());
+  launch_pdl(bmm_tc_kernel, grid, dim3(bmmtc::kThreads), (size_t)smem, st, p);
   note_tc_launch(e.mode == EPI_BITS ? "bmm_packed/bin" : e.mode == EPI_F64 ? "bmm_packed/bn" : "bmm_packed/i32",
                  (int)(grid.x * grid.y), (int)(grid.x * grid.y));
 }

@@ -317,7 +317,9 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     launch_input_rows(d_x, batch * plan->in_h, (int)(plan->in_w * plan->in_c), sh.flag.get<int>(),
                       sh.rowmax.get<uint32_t>(), st);
     ++launches;
-  } else {
+  } else if ((sh.layers[0].spec.kind != BTNN_BIT_FC && sh.layers[0].spec.kind != BTNN_LAST_FC) ||
+             sh.layers[0].spec.in_channels != plan->in_h * plan->in_w * plan->in_c) {
+    // (an FC-first model's pack_rows pass checks every input value itself)
     launch_check_finite(d_x, batch * plan->in_h * plan->in_w * plan->in_c, sh.flag.get<int>(), st);
     ++launches;
   }
@@ -448,8 +450,8 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         uint64_t* dst = sh.fc[fcur].get<uint64_t>();
         const size_t row_words = ru(l.in_channels, 128) / 64;
         if (i == 0) {
-          // FC-first model: binarize the raw input (inference.hpp:149-151); non-finite
-          // values were already flagged by the input check.
+          // FC-first model: binarize the raw input (inference.hpp:149-151) and flag
+          // non-finite values (the input check of inference.hpp:69-75, no separate pass).
           BT_CUDA(cudaMemsetAsync(dst, 0, batch * row_words * 8, st));
           launch_pack_rows(d_x, batch, l.in_channels, row_words * 2, reinterpret_cast<uint32_t*>(dst),
                            sh.flag.get<int>(), st);
