@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <atomic>
 #include <cstdint>
 
@@ -49,6 +50,7 @@ struct BmmTcArgs {
   int cwo32;               // output words (32-bit) per row
   const long long* thr_lo;  // EPI_BITS: per column lo / hi (nullptr: v >= 0)
   const long long* thr_hi;
+  int32_t* labels;      // EPI_F64, N <= 64 (whole-K kernel): each row's argmax written too
   const uint8_t* bpre;  // pipelined kernel, PRE: B expanded to {0,1} blocks (bmm_expand_b01_kernel)
 };
 
@@ -280,6 +282,21 @@ __global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid
           if (n0 + cc < p.N) dst[0] = v.x;
           if (n0 + cc + 1 < p.N) dst[1] = v.y;
         }
+        if (p.labels) {
+          // the row's first-index argmax, as argmax_kernel / the sequential scan
+          // (inference.hpp:177-184): every column of the row is in this tile (N <= 64)
+          double bv = -INFINITY;
+          int bi = INT_MAX;
+          if (cc < p.N) { bv = v.x; bi = cc; }
+          if (cc + 1 < p.N && (bi == INT_MAX || v.y > bv)) { bv = v.y; bi = cc + 1; }
+#pragma unroll
+          for (int off = 16; off; off >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+          }
+          if (lane == 0) p.labels[orow] = bi;
+        }
       }
     } else {
       // through shared memory (B's expanded tile is dead once the MMAs completed): rows of 64
@@ -328,6 +345,10 @@ __global__ void __launch_bounds__(bmmtc::kThreads, 1) bmm_tc_kernel(const __grid
 // output (EPI_I32 raw / pm1 into out_i32, EPI_BITS into out_bits with optional thresholds).
 void launch_bmm_tc(int M, int N, int K, const uint64_t* a, const uint64_t* b, const Epi& e, cudaStream_t st) {
   BmmTcArgs p{};
+  if (e.mode == EPI_F64 && e.labels && N <= bmmtc::kBN) {  // fused argmax
+    p.labels = e.labels;
+    if (e.labels_done) *e.labels_done = true;
+  }
   p.a = a;
   p.b = b;
   p.M = M;

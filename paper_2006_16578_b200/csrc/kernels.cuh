@@ -49,6 +49,8 @@ struct Epi {
                                      //   tensor-core engine split few-tile FC GEMMs along K
   double* rout_half = nullptr;       // residual_out pre-averaged for a halving consumer,
                                      //   PQNO over (P/2, Q/2, N, O) (tensor-core engine only)
+  int32_t* labels = nullptr;         // EPI_F64 (the last layer): kernels that can also write each
+  bool* labels_done = nullptr;       //   row's argmax set *labels_done (host flag, at launch)
   int pool = 0;                      // fused or_pool (bconv.hpp:247-272) with window = stride = pool:
                                      //   bits are OR-ed (atomicOr) into the pooled site (p/pool, q/pool)
                                      //   of a zeroed (P/pool, Q/pool) tensor (tensor-core engine only)

@@ -324,6 +324,7 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
     ++launches;
   }
   const size_t np = act_npad(batch, 0, 0);
+  bool labels_done = false;  // the last layer's kernel wrote the argmax labels
   int cur = 0;              // act buffer holding the current activations
   int fcur = 0;             // fc buffer holding the current fc activations
   bool in_fc = false;
@@ -481,14 +482,20 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         e.bn_rcp = e.bn_mean + 4 * O;
         e.rout = d_logits;  // logits = bn(v) (inference.hpp:161-164)
         e.split_ws = L.split_ws.get<int32_t>();
+        if (i + 1 == sh.layers.size() && !timed) {  // the packed BMM may write the labels too
+          e.labels = d_labels;
+          e.labels_done = &labels_done;
+        }
         L.engine = launch_bgemm(s, sh.fc[fcur].get<uint64_t>(), L.filt.get<uint64_t>(), e, st, EngineHint::Auto, &L.tc);
       }
       launches += L.engine == std::string("tc_i8_splitk") ? 2 : 1;
     }
   }
   if (timed) BT_CUDA(cudaEventRecord(sh.events[sh.layers.size()], st));
-  launch_argmax(d_logits, (int)batch, (int)plan->classes, d_labels, st);
-  ++launches;
+  if (!labels_done) {
+    launch_argmax(d_logits, (int)batch, (int)plan->classes, d_labels, st);
+    ++launches;
+  }
   return launches;
 }
 
