@@ -7,6 +7,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "umma.cuh"
 #include "layout.cuh"
 
 namespace btnn_gpu {
@@ -399,10 +400,12 @@ void launch_check_finite(const float* x, size_t n, int* flag, cudaStream_t st) {
 }
 
 // One warp per 32 consecutive columns of a row: bit = x >= 0 (bit_buffer.hpp:83), pad
-// columns stay 0, the ballot is the 32-bit word.
+// columns 0, the ballot is the 32-bit word; every word of the padded row is written (no
+// clearing pass). The next kernel may launch early (it waits for this grid's writes).
 __global__ void pack_rows_kernel(const float* __restrict__ x, size_t rows, size_t cols, size_t row_words32,
                                  uint32_t* out, int* nonfinite) {
-  const size_t cols32 = (cols + 31) / 32 * 32;
+  umma::grid_dep_launch();
+  const size_t cols32 = row_words32 * 32;
   const size_t total = rows * cols32;
   for (size_t base = (size_t)blockIdx.x * blockDim.x; base < total; base += (size_t)gridDim.x * blockDim.x) {
     const size_t idx = base + threadIdx.x;
@@ -423,7 +426,7 @@ __global__ void pack_rows_kernel(const float* __restrict__ x, size_t rows, size_
 }
 void launch_pack_rows(const float* x, size_t rows, size_t cols, size_t row_words32, uint32_t* out,
                       int* nonfinite, cudaStream_t st) {
-  const size_t total = rows * ((cols + 31) / 32 * 32);
+  const size_t total = rows * row_words32 * 32;
   if (!total) return;
   const size_t blocks = (total + 255) / 256;
   pack_rows_kernel<<<(unsigned)(blocks < 148 * 32 ? blocks : 148 * 32), 256, 0, st>>>(x, rows, cols, row_words32,

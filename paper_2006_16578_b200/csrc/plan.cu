@@ -453,7 +453,6 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
         if (i == 0) {
           // FC-first model: binarize the raw input (inference.hpp:149-151) and flag
           // non-finite values (the input check of inference.hpp:69-75, no separate pass).
-          BT_CUDA(cudaMemsetAsync(dst, 0, batch * row_words * 8, st));
           launch_pack_rows(d_x, batch, l.in_channels, row_words * 2, reinterpret_cast<uint32_t*>(dst),
                            sh.flag.get<int>(), st);
         } else {
@@ -467,7 +466,9 @@ static size_t enqueue_forward(btnn_plan* plan, Shard& sh, const float* d_x, size
       Epi e;
       if (l.kind == BTNN_BIT_FC) {
         uint64_t* out = sh.fc[fcur ^ 1].get<uint64_t>();
-        BT_CUDA(cudaMemsetAsync(out, 0, batch * (size_t)s.cwo * 8, st));
+        // every engine writes whole 64-bit words of its output columns: only rows with pad
+        // words past O need clearing
+        if (s.O % 128) BT_CUDA(cudaMemsetAsync(out, 0, batch * (size_t)s.cwo * 8, st));
         e.mode = EPI_BITS;
         e.out_bits = out;
         e.thr_lo = L.thr_lo.get<long long>();
