@@ -545,7 +545,8 @@ def run_model(a, rank, world, local, dist):
                "e2e": {"value": e2e, "unit": unit, "h2d_bytes_per_step": int(xh.numel() * 4),
                        "d2h_bytes_per_step": int(lh.numel() * 8 + bh.numel() * 4),
                        "h2d_ceiling_gbs": h2d, "h2d_ceiling_img_s": h2d * 1e9 / (in_bytes / B),
-                       "frac_of_h2d_ceiling": e2e / (h2d * 1e9 / (in_bytes / B))},
+                       "frac_of_h2d_ceiling": e2e / (h2d * 1e9 / (in_bytes / B)),
+                       "pipeline": plan.e2e_schedule(B)},
                "gpu_launches": launches * a.steps,
                "roofline": roof,
                "parity": parity,

@@ -308,6 +308,12 @@ int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size
  * run's input held a non-finite value — the condition under which run_inference throws
  * invalid_input (inference.hpp:69-75); the device run's logits are then not the reference's. */
 int btnn_cuda_plan_input_status(btnn_plan* plan, int shard, int* nonfinite);
+/* End-to-end input pipelining of btnn_cuda_plan_run (the host-buffer run_inference): the chunk
+ * sizes shard `shard` uses for `batch` images (n_sizes of them, the first `cap` written) and its
+ * measured model: model[0] = 1 once calibrated (on the shard's first host run), [1] host->device
+ * copy us per image, [2] graph latency t0 us, [3] graph us per image, [4] the modelled step us. */
+int btnn_cuda_plan_e2e_schedule(btnn_plan* plan, int shard, size_t batch, double* model, size_t* sizes, size_t cap,
+                                size_t* n_sizes);
 /* Per-layer device time of the last plan_run on shard 0, ms (RunOptions::breakdown,
  * inference.hpp:169-174). n_layers entries. */
 int btnn_cuda_plan_layer_ms(btnn_plan* plan, double* ms, size_t n_layers);

@@ -262,6 +262,18 @@ class Plan:
         check(lib().btnn_cuda_plan_input_status(self.h, shard, C.byref(f)))
         return bool(f.value)
 
+    def e2e_schedule(self, batch: int, shard: int = 0):
+        """The input pipelining run() uses for `batch` images on `shard`: chunk sizes and the
+        measured model behind them (None before the shard's first host run calibrated it)."""
+        model = (C.c_double * 5)()
+        sizes = (C.c_size_t * 32)()
+        n = C.c_size_t()
+        check(lib().btnn_cuda_plan_e2e_schedule(self.h, shard, batch, model, sizes, 32, C.byref(n)))
+        if not model[0]:
+            return None
+        return {"chunks": [int(sizes[i]) for i in range(min(n.value, 32))], "copy_us_per_image": model[1],
+                "graph_t0_us": model[2], "graph_us_per_image": model[3], "modelled_step_us": model[4]}
+
     def set_breakdown(self, on: bool):
         check(lib().btnn_cuda_plan_set_breakdown(self.h, int(on)))
 

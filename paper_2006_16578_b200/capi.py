@@ -141,6 +141,7 @@ _PROTOS = {
     "btnn_cuda_plan_destroy": (C.c_int, [C.c_void_p]),
     "btnn_cuda_set_autotune": (C.c_int, [C.c_int]),
     "btnn_cuda_plan_input_status": (C.c_int, [C.c_void_p, C.c_int, P(C.c_int)]),
+    "btnn_cuda_plan_e2e_schedule": (C.c_int, [C.c_void_p, C.c_int, sz, P(C.c_double), P(sz), sz, P(sz)]),
     "btnn_cuda_plan_set_layer_choice": (C.c_int, [C.c_void_p, sz, sz]),
     "btnn_cuda_plan_layer_choice": (C.c_int, [C.c_void_p, sz, C.c_char_p, sz, P(C.c_double), sz]),
     "btnn_cuda_benn_combine": (C.c_int, [C.c_void_p, C.c_void_p, sz, sz, sz, C.POINTER(C.c_double), C.c_int,

@@ -73,7 +73,13 @@ struct Shard {
   std::map<std::tuple<size_t, const void*, const void*, const void*, int>, Graph> graphs;
   std::vector<cudaEvent_t> events;  // breakdown
   cudaStream_t copy_stream = nullptr;    // host->device input chunks (run_shard_host)
+  cudaStream_t d2h_stream = nullptr;     // device->host results per chunk (pinned outputs)
   std::vector<cudaEvent_t> in_ready;     // per chunk: input resident
+  std::vector<cudaEvent_t> out_ready;    // per chunk: logits / labels computed
+  // e2e chunk model (calibrate_e2e, measured once per shard on its first host run): host ->
+  // device copy time per image (us) and the graph's time t(b) = t0 + b * s (us) for b images
+  bool e2e_cal = false;
+  double e2e_c = 0.0, e2e_t0 = 0.0, e2e_s = 0.0;
   size_t launches = 0;
   int tune_pass = -1;  // >= 0 while tune_shard runs candidate pass k of every layer
   ~Shard() {
@@ -81,6 +87,8 @@ struct Shard {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
     for (auto ev : events) cudaEventDestroy(ev);
     for (auto ev : in_ready) cudaEventDestroy(ev);
+    for (auto ev : out_ready) cudaEventDestroy(ev);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
   }
@@ -177,6 +185,7 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
   BT_CUDA(cudaSetDevice(sh.device));
   BT_CUDA(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
   BT_CUDA(cudaStreamCreateWithFlags(&sh.copy_stream, cudaStreamNonBlocking));
+  BT_CUDA(cudaStreamCreateWithFlags(&sh.d2h_stream, cudaStreamNonBlocking));
   cudaStream_t st = sh.stream;
   const size_t B = sh.max_batch;
   sh.layers.resize(m->n_layers);
@@ -274,6 +283,8 @@ static void build_shard(Shard& sh, const btnn_model_spec* m, const btnn_weight_s
   for (auto& ev : sh.events) BT_CUDA(cudaEventCreate(&ev));
   sh.in_ready.resize(kMaxChunks);
   for (auto& ev : sh.in_ready) BT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  sh.out_ready.resize(kMaxChunks);
+  for (auto& ev : sh.out_ready) BT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   BT_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -536,45 +547,133 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
 // Host-buffer run (the C ABI's run_inference). The input copy is the long pole end to end
 // (602 KB per ImageNet image over PCIe, ~55 GB/s measured: ~90 K img/s), so the batch is cut
 // into chunks: chunk k+1's host->device copy runs on the copy stream while chunk k's graph
-// runs on the compute stream. Samples are independent, so chunking does not change any result.
+// runs on the compute stream, and chunk k's logits / labels go back to the host right behind
+// its graph. Samples are independent, so chunking does not change any result.
 //
-// The step ends when the last chunk's copy and then its compute finish. Big chunks run the
-// network efficiently (a 128-image graph computes ~1.4x faster than its copy arrives; a
-// 64-image one barely keeps pace) while a small last chunk keeps the exposed compute tail
-// short, so the schedule takes chunks of up to 128 images while more than two remain, then
-// halves them down to 16: batch 512 -> 128 128 128 64 32 16 16.
-static std::vector<size_t> chunk_schedule(size_t batch, size_t in_bytes_per_image) {
-  std::vector<size_t> sizes;
+// The schedule comes from measurements, not constants (calibrate_e2e): the copy time per image
+// c from a timed copy of the caller's own buffer, and the graph's time t(b) = t0 + b * s from
+// two timed replays (ResNet-18 on a B200: t0 ~ 0.29 ms, s ~ 4.8 us, c ~ 10.9 us). The step ends
+// when the last chunk's copy and then its compute finish, so the last chunk wants to be small —
+// but a chunk's graph must also finish before the next chunk's copy does, or the compute stream
+// backs up: walking backwards, chunk k may be as large as (b_{k+1} * c - t0) / s, so chunks
+// grow geometrically from a small last one. Every candidate (each last-chunk size, uniform
+// chunks, one chunk) is simulated with the model and the fastest kept.
+static bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// kChunkIssueUs: host issue cost of one chunk (copy, event record and wait, graph launch, two
+// result copies: ~6 runtime calls), which paces the pipeline when a chunk's device work is
+// short (MNIST-MLP: ~20 us graphs).
+constexpr double kChunkIssueUs = 25.0;
+static double simulate_chunks(const std::vector<size_t>& sizes, double c, double t0, double s) {
+  double copy_done = 0.0, comp_end = 0.0, issued = 0.0;
+  for (size_t b : sizes) {
+    issued += kChunkIssueUs;
+    copy_done = std::max(copy_done, issued) + (double)b * c;
+    comp_end = std::max(copy_done, comp_end) + t0 + (double)b * s;
+  }
+  return comp_end;
+}
+
+static std::vector<size_t> chunk_schedule(const Shard& sh, size_t batch) {
   static const size_t fixed = (size_t)timing_knob("BTNN_E2E_CHUNK", 0);  // timing experiments
   if (fixed) {
+    std::vector<size_t> sizes;
     for (size_t b0 = 0; b0 < batch; b0 += fixed) sizes.push_back(std::min(fixed, batch - b0));
     return sizes;
   }
-  // Small batches are latency-bound, and small inputs (Cifar 12 KB, MNIST 3 KB per image)
-  // copy in a fraction of the compute time: one graph each.
-  if (batch < 128 || in_bytes_per_image < 64 * 1024) return {batch};
-  // (large batches: bigger base chunks so the whole schedule fits kMaxChunks events)
-  const size_t base = std::max<size_t>({16, std::min<size_t>(128, ru(batch / 4, 8)), ru(batch / 12, 8)});
-  size_t r = batch;
-  while (r > 2 * base && sizes.size() + 6 < kMaxChunks) {
-    sizes.push_back(base);
-    r -= base;
+  if (!sh.e2e_cal || batch < 16) return {batch};
+  const double c = sh.e2e_c, t0 = sh.e2e_t0, sl = sh.e2e_s;
+  std::vector<size_t> best{batch};
+  double best_t = simulate_chunks(best, c, t0, sl);
+  auto consider = [&](std::vector<size_t> v) {
+    if (v.empty() || v.size() > kMaxChunks) return;
+    const double t = simulate_chunks(v, c, t0, sl);
+    if (t < best_t) best_t = t, best = std::move(v);
+  };
+  const size_t cap = std::min<size_t>(batch, 512);
+  for (size_t last = 8; last <= std::min<size_t>(batch, 256); last += 8) {
+    // backwards from the last chunk: each earlier chunk as large as its successor's copy hides
+    std::vector<size_t> rev{last};
+    size_t tot = last;
+    while (tot < batch && rev.size() < kMaxChunks) {
+      const double lim = ((double)rev.back() * c - t0) / sl;
+      size_t b = lim <= (double)rev.back() ? 2 * rev.back() : (size_t)lim / 8 * 8;  // (compute-bound: double)
+      b = std::max<size_t>(8, std::min(b, cap));
+      b = std::min(b, batch - tot);
+      rev.push_back(b);
+      tot += b;
+    }
+    if (tot < batch) continue;
+    consider(std::vector<size_t>(rev.rbegin(), rev.rend()));
   }
-  while (r > 16 && sizes.size() + 2 < kMaxChunks) {
-    const size_t c = std::min(r, ru(cdiv(r, 2), 8));
-    sizes.push_back(c);
-    r -= c;
+  for (size_t u = 16; u <= std::min<size_t>(batch, 256); u += 16) {  // uniform chunks
+    std::vector<size_t> v;
+    for (size_t b0 = 0; b0 < batch; b0 += u) v.push_back(std::min(u, batch - b0));
+    consider(v);
   }
-  if (r) sizes.push_back(r);
-  return sizes;
+  return best;
+}
+
+// One-time measurement of the chunk model on the caller's buffer (first host run of a shard):
+// a timed copy of up to 64 images (after one untimed), and two timed replays of the graph at
+// b = 16 and b = 128 (or the largest batch the shard holds) on whatever the device input buffer
+// holds — the graph's speed does not depend on the values; any non-finite flag raised here is
+// cleared by the run that follows.
+static void calibrate_e2e(btnn_plan* plan, Shard& sh, const float* x, size_t batch) {
+  const size_t xin = plan->in_h * plan->in_w * plan->in_c;
+  cudaEvent_t e0, e1;
+  BT_CUDA(cudaEventCreate(&e0));
+  BT_CUDA(cudaEventCreate(&e1));
+  auto elapsed_us = [&](cudaStream_t st) {
+    BT_CUDA(cudaEventRecord(e1, st));
+    BT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    BT_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    return 1e3 * (double)ms;
+  };
+  const size_t nb = std::min<size_t>(batch, 64);
+  const size_t b1 = std::min<size_t>(16, sh.max_batch), b2 = std::min<size_t>(128, sh.max_batch);
+  BT_CUDA(cudaMemsetAsync(sh.x.get(), 0, b2 * xin * sizeof(float), sh.copy_stream));  // (finite values)
+  BT_CUDA(cudaMemcpyAsync(sh.x.get(), x, nb * xin * sizeof(float), cudaMemcpyHostToDevice, sh.copy_stream));
+  BT_CUDA(cudaEventRecord(e0, sh.copy_stream));
+  BT_CUDA(cudaMemcpyAsync(sh.x.get(), x, nb * xin * sizeof(float), cudaMemcpyHostToDevice, sh.copy_stream));
+  const double c = elapsed_us(sh.copy_stream) / (double)nb;
+  double t[2] = {0.0, 0.0};
+  const size_t bs[2] = {b1, b2};
+  for (int i = 0; i < 2; ++i) {
+    run_shard_device(plan, sh, sh.x.get<float>(), bs[i], sh.logits.get<double>(), sh.labels.get<int32_t>(), false);
+    BT_CUDA(cudaEventRecord(e0, sh.stream));
+    run_shard_device(plan, sh, sh.x.get<float>(), bs[i], sh.logits.get<double>(), sh.labels.get<int32_t>(), false);
+    t[i] = elapsed_us(sh.stream);
+  }
+  BT_CUDA(cudaEventDestroy(e0));
+  BT_CUDA(cudaEventDestroy(e1));
+  const double sl = b2 > b1 ? std::max(0.0, (t[1] - t[0]) / (double)(b2 - b1)) : t[0] / (double)b1;
+  sh.e2e_c = c;
+  sh.e2e_s = sl;
+  sh.e2e_t0 = std::max(0.0, t[0] - sl * (double)b1);
+  sh.e2e_cal = true;
 }
 
 static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t batch, double* logits, int32_t* labels) {
   BT_CUDA(cudaSetDevice(sh.device));
   const size_t xin = plan->in_h * plan->in_w * plan->in_c;
   const bool timed = plan->breakdown && &sh == plan->shards[0].get();
-  const std::vector<size_t> sizes = timed ? std::vector<size_t>{batch} : chunk_schedule(batch, xin * sizeof(float));
+  // Small inputs (Cifar 12 KB, MNIST 3 KB per image) copy in a fraction of the compute time and
+  // each extra chunk costs more host and launch time than it hides (measured: Cifar-VGG b1024
+  // 684 K -> 538 K img/s, MNIST-MLP 4.3 M -> 2.7 M with 3-4 chunks): one graph each.
+  const bool pipelined = batch >= 16 && xin * sizeof(float) >= 64 * 1024;
+  if (!timed && pipelined && !sh.e2e_cal && !timing_knob("BTNN_E2E_CHUNK", 0)) calibrate_e2e(plan, sh, x, batch);
+  const std::vector<size_t> sizes = timed || !pipelined ? std::vector<size_t>{batch} : chunk_schedule(sh, batch);
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
+  const bool pinned_out = sizes.size() > 1 && host_pinned(logits) && host_pinned(labels);
   size_t b0 = 0;
   for (size_t k = 0; k < sizes.size(); ++k) {
     const size_t bn = sizes[k];
@@ -582,16 +681,27 @@ static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t ba
     BT_CUDA(cudaMemcpyAsync(dx, x + b0 * xin, bn * xin * sizeof(float), cudaMemcpyHostToDevice, sh.copy_stream));
     BT_CUDA(cudaEventRecord(sh.in_ready[k], sh.copy_stream));
     BT_CUDA(cudaStreamWaitEvent(sh.stream, sh.in_ready[k], 0));
-    run_shard_device(plan, sh, dx, bn, sh.logits.get<double>() + b0 * plan->classes, sh.labels.get<int32_t>() + b0,
-                     timed);
+    double* dl = sh.logits.get<double>() + b0 * plan->classes;
+    int32_t* db = sh.labels.get<int32_t>() + b0;
+    run_shard_device(plan, sh, dx, bn, dl, db, timed);
+    if (pinned_out) {  // this chunk's results leave (own stream) while the next chunk computes
+      BT_CUDA(cudaEventRecord(sh.out_ready[k], sh.stream));
+      BT_CUDA(cudaStreamWaitEvent(sh.d2h_stream, sh.out_ready[k], 0));
+      BT_CUDA(cudaMemcpyAsync(logits + b0 * plan->classes, dl, bn * plan->classes * sizeof(double),
+                              cudaMemcpyDeviceToHost, sh.d2h_stream));
+      BT_CUDA(cudaMemcpyAsync(labels + b0, db, bn * sizeof(int32_t), cudaMemcpyDeviceToHost, sh.d2h_stream));
+    }
     b0 += bn;
+  }
+  if (!pinned_out) {  // (a copy to pageable memory blocks the host: once, at the end)
+    BT_CUDA(cudaMemcpyAsync(logits, sh.logits.get(), batch * plan->classes * sizeof(double), cudaMemcpyDeviceToHost,
+                            sh.stream));
+    BT_CUDA(cudaMemcpyAsync(labels, sh.labels.get(), batch * sizeof(int32_t), cudaMemcpyDeviceToHost, sh.stream));
   }
   int bad = 0;
   BT_CUDA(cudaMemcpyAsync(&bad, sh.flag.get(), sizeof(int), cudaMemcpyDeviceToHost, sh.stream));
-  BT_CUDA(cudaMemcpyAsync(logits, sh.logits.get(), batch * plan->classes * sizeof(double), cudaMemcpyDeviceToHost,
-                          sh.stream));
-  BT_CUDA(cudaMemcpyAsync(labels, sh.labels.get(), batch * sizeof(int32_t), cudaMemcpyDeviceToHost, sh.stream));
   BT_CUDA(cudaStreamSynchronize(sh.stream));
+  if (pinned_out) BT_CUDA(cudaStreamSynchronize(sh.d2h_stream));
   require(!bad, BTNN_INVALID_INPUT, "run_inference: non-finite input");
   if (plan->breakdown && &sh == plan->shards[0].get()) {
     plan->layer_ms.assign(sh.layers.size(), 0.0);
@@ -780,6 +890,23 @@ int btnn_cuda_plan_run_device(btnn_plan* plan, int shard, const float* d_x, size
     BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), ls));
     run_shard_device(plan, sh, d_x, batch, d_logits ? d_logits : sh.logits.get<double>(),
                      d_labels ? d_labels : sh.labels.get<int32_t>(), false, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int btnn_cuda_plan_e2e_schedule(btnn_plan* plan, int shard, size_t batch, double* model, size_t* sizes, size_t cap,
+                                size_t* n_sizes) {
+  return guard([&] {
+    require(plan && shard >= 0 && (size_t)shard < plan->shards.size() && model && sizes && n_sizes, BTNN_INVALID_INPUT,
+            "plan_e2e_schedule: bad arguments");
+    const Shard& sh = *plan->shards[shard];
+    model[0] = sh.e2e_cal ? 1.0 : 0.0;
+    model[1] = sh.e2e_c;
+    model[2] = sh.e2e_t0;
+    model[3] = sh.e2e_s;
+    const std::vector<size_t> v = chunk_schedule(sh, batch);
+    model[4] = sh.e2e_cal ? simulate_chunks(v, sh.e2e_c, sh.e2e_t0, sh.e2e_s) : 0.0;
+    *n_sizes = v.size();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) sizes[i] = v[i];
   });
 }
 

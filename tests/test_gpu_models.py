@@ -264,3 +264,38 @@ def test_fused_input_check_of_stride4_first_conv(engine):
         assert plan.input_status()
     lg2, _ = plan.run(x)
     assert np.array_equal(lg2.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("name,hw,batch", [("mnist-mlp", 128, 200), ("mnist-mlp", 28, 333)])
+def test_e2e_chunked_pipeline_pinned_and_pageable(name, hw, batch):
+    """plan_run's measured input pipelining (chunk schedule from the calibrated copy / graph
+    model; per-chunk result copies on their own stream when the host buffers are pinned):
+    pinned and pageable host buffers both give the oracle's logits, whatever the schedule."""
+    import ctypes as C
+
+    import torch
+
+    m = M.stock_model(name, hw, hw)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 3))
+    x = np.random.default_rng(4).standard_normal((batch, m.in_h, m.in_w, m.in_c), dtype=np.float32)
+    plan = B.Plan(m, ws, batch)
+    lg, lb = plan.run(x)  # pageable (numpy) buffers; the first host run calibrates the model
+    sched = plan.e2e_schedule(batch)
+    if m.in_h * m.in_w * m.in_c * 4 >= 64 * 1024:  # pipelined: a measured multi-chunk schedule
+        assert sched is not None and sum(sched["chunks"]) == batch and all(c > 0 for c in sched["chunks"])
+    else:  # small inputs: one graph, no calibration
+        assert sched is None
+    xh = torch.from_numpy(x).pin_memory()
+    lh = torch.zeros((batch, m.classes), dtype=torch.float64).pin_memory()
+    bh = torch.zeros((batch,), dtype=torch.int32).pin_memory()
+    for k in range(2):
+        capi.check(capi.lib().btnn_cuda_plan_run(plan.h, C.cast(xh.data_ptr(), C.POINTER(C.c_float)), batch,
+                                                 C.cast(lh.data_ptr(), C.POINTER(C.c_double)),
+                                                 C.cast(bh.data_ptr(), C.POINTER(C.c_int32))))
+        assert np.array_equal(lh.numpy().view(np.uint64), lg.view(np.uint64)), (k, sched)
+        assert np.array_equal(bh.numpy(), lb)
+        lh.zero_()
+        bh.zero_()
+    want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+    assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(lb, wl)
