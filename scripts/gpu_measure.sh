@@ -16,7 +16,7 @@ for m in alexnet cifar-vgg mnist-mlp bmm1024; do
 done
 timeout 600 python bench.py --model cifar-vgg --batch 256 > $O/bench_cifar-vgg_b256.json 2> $O/bench_cifar-vgg_b256.err
 if [ -z "$NOSUITES" ]; then
-  for s in bmm bmm-bin bconv bconv-bin; do timeout 600 python scripts/bench_suites.py --suite $s --csv $O/suite_$s.csv > /dev/null 2>&1; echo "suite $s rc=$?"; done
+  for s in bmm bmm-bin bconv bconv-bin; do timeout 900 python scripts/bench_suites.py --suite $s --bmm-max-n 16384 --csv $O/suite_$s.csv > /dev/null 2>&1; echo "suite $s rc=$?"; done
   timeout 600 python scripts/bench_suites.py --suite model --model resnet18 --batches 8,64,256,512,1024,2048,4096 --csv $O/suite_model_resnet18.csv > /dev/null 2>&1; echo "suite model rc=$?"
 fi
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_resnet18_b512.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-kernels > $O/ncu_l.log 2>&1; echo "ncu-l rc=$?"
