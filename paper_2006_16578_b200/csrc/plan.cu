@@ -558,6 +558,9 @@ static void run_shard_device(btnn_plan* plan, Shard& sh, const float* d_x, size_
 // backs up: walking backwards, chunk k may be as large as (b_{k+1} * c - t0) / s, so chunks
 // grow geometrically from a small last one. Every candidate (each last-chunk size, uniform
 // chunks, one chunk) is simulated with the model and the fastest kept.
+#ifndef BTNN_E2E_MIN_BYTES
+#define BTNN_E2E_MIN_BYTES (64 * 1024)
+#endif
 static bool host_pinned(const void* p) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -667,9 +670,10 @@ static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t ba
   const size_t xin = plan->in_h * plan->in_w * plan->in_c;
   const bool timed = plan->breakdown && &sh == plan->shards[0].get();
   // Small inputs (Cifar 12 KB, MNIST 3 KB per image) copy in a fraction of the compute time and
-  // each extra chunk costs more host and launch time than it hides (measured: Cifar-VGG b1024
-  // 684 K -> 538 K img/s, MNIST-MLP 4.3 M -> 2.7 M with 3-4 chunks): one graph each.
-  const bool pipelined = batch >= 16 && xin * sizeof(float) >= 64 * 1024;
+  // each extra chunk costs more host and launch time than it hides (measured with the model's
+  // schedules, XDEFS=-DBTNN_E2E_MIN_BYTES=0: Cifar-VGG b1024 700 K -> 668 K img/s, MNIST-MLP
+  // 7.7 M -> 5.8 M with 3-4 chunks): one graph each.
+  const bool pipelined = batch >= 16 && xin * sizeof(float) >= BTNN_E2E_MIN_BYTES;
   if (!timed && pipelined && !sh.e2e_cal && !timing_knob("BTNN_E2E_CHUNK", 0)) calibrate_e2e(plan, sh, x, batch);
   const std::vector<size_t> sizes = timed || !pipelined ? std::vector<size_t>{batch} : chunk_schedule(sh, batch);
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
