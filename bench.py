@@ -534,6 +534,19 @@ def run_model(a, rank, world, local, dist):
     top = int(np.argmax(layer_ms))
     roof = roofline(m, B, top, layer_ms[top], engines[top], plan)
     roof["share_of_step"] = float(layer_ms[top] / layer_ms.sum())
+    # every layer against its own bound; the network's composite roofline fraction is the time
+    # the layers would take at their bounds over the time they take (layers without a bound:
+    # their measured time counts on both sides)
+    per_layer, ideal = [], 0.0
+    for i, L in enumerate(m.layers):
+        # (an or_pool fused into its producer's epilogue does no work of its own)
+        r = roofline(m, B, i, layer_ms[i], engines[i], plan) if layer_ms[i] > 0 and engines[i] != "fused" else {}
+        f = r.get("frac")
+        per_layer.append({"layer": i, "engine": engines[i], "ms": float(layer_ms[i]), "bound": r.get("bound"),
+                          "achieved": r.get("achieved"), "unit": r.get("unit"), "frac": f})
+        ideal += layer_ms[i] * (f if f else 1.0)
+    network_roofline = {"frac": float(ideal / layer_ms.sum()), "ideal_ms": float(ideal),
+                        "measured_ms": float(layer_ms.sum()), "layers": per_layer}
     tr = measured_traffic(f"{a.model}:layer{top}:{engines[top]}") or (
         measured_traffic(f"layer{top}:{engines[top]}") if a.model == "resnet18" else None)
     if tr is not None:  # DRAM bytes per launch from the committed ncu capture, scaled to B
@@ -563,6 +576,7 @@ def run_model(a, rank, world, local, dist):
                        "pipeline": plan.e2e_schedule(B), "steps": e2e_steps, "warmup": e2e_warm},
                "gpu_launches": launches * a.steps,
                "roofline": roof,
+               "network_roofline": network_roofline,
                "parity": parity,
                "layer_ms": {f"{i}:{engines[i]}": round(float(t), 4) for i, t in enumerate(layer_ms)},
                "paper_turing_img_s": PAPER_IMG_S.get(a.model),
