@@ -266,7 +266,7 @@ def test_fused_input_check_of_stride4_first_conv(engine):
     assert np.array_equal(lg2.view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("name,hw,batch", [("mnist-mlp", 128, 200), ("mnist-mlp", 28, 333)])
+@pytest.mark.parametrize("name,hw,batch", [("mnist-mlp", 128, 200), ("mnist-mlp", 128, 37), ("mnist-mlp", 28, 333)])
 def test_e2e_chunked_pipeline_pinned_and_pageable(name, hw, batch):
     """plan_run's measured input pipelining (chunk schedule from the calibrated copy / graph
     model; per-chunk result copies on their own stream when the host buffers are pinned):
