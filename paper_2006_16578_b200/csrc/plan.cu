@@ -79,6 +79,7 @@ struct Shard {
   // e2e chunk model (calibrate_e2e, measured once per shard on its first host run): host ->
   // device copy time per image (us) and the graph's time t(b) = t0 + b * s (us) for b images
   bool e2e_cal = false;
+  bool e2e_cal_pinned = false;  // the input buffer kind the model was measured on
   double e2e_c = 0.0, e2e_t0 = 0.0, e2e_s = 0.0;
   size_t launches = 0;
   int tune_pass = -1;  // >= 0 while tune_shard runs candidate pass k of every layer
@@ -674,7 +675,13 @@ static void run_shard_host(btnn_plan* plan, Shard& sh, const float* x, size_t ba
   // schedules, XDEFS=-DBTNN_E2E_MIN_BYTES=0: Cifar-VGG b1024 700 K -> 668 K img/s, MNIST-MLP
   // 7.7 M -> 5.8 M with 3-4 chunks): one graph each.
   const bool pipelined = batch >= 16 && xin * sizeof(float) >= BTNN_E2E_MIN_BYTES;
-  if (!timed && pipelined && !sh.e2e_cal && !timing_knob("BTNN_E2E_CHUNK", 0)) calibrate_e2e(plan, sh, x, batch);
+  // (re-measured when the caller switches between pinned and pageable input buffers: the copy
+  // rate differs by ~2-4x)
+  const bool x_pinned = pipelined && host_pinned(x);
+  if (!timed && pipelined && (!sh.e2e_cal || sh.e2e_cal_pinned != x_pinned) && !timing_knob("BTNN_E2E_CHUNK", 0)) {
+    calibrate_e2e(plan, sh, x, batch);
+    sh.e2e_cal_pinned = x_pinned;
+  }
   const std::vector<size_t> sizes = timed || !pipelined ? std::vector<size_t>{batch} : chunk_schedule(sh, batch);
   BT_CUDA(cudaMemsetAsync(sh.flag.get(), 0, sizeof(int), sh.stream));
   const bool pinned_out = sizes.size() > 1 && host_pinned(logits) && host_pinned(labels);
