@@ -299,3 +299,20 @@ def test_e2e_chunked_pipeline_pinned_and_pageable(name, hw, batch):
     want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
     assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
     assert np.array_equal(lb, wl)
+
+
+def test_e2e_pipeline_two_shards():
+    """Two shards on device 0 (two host threads), each calibrating and pipelining its half of a
+    large-input batch: the oracle's logits."""
+    m = M.stock_model("mnist-mlp", 128, 128)
+    ws = Wt.build_weights(m, Wt.random_weights(m, 5))
+    x = np.random.default_rng(6).standard_normal((150, m.in_h, m.in_w, m.in_c), dtype=np.float32)
+    plan = B.Plan(m, ws, 150, devices=(0, 0))
+    for _ in range(2):
+        lg, lb = plan.run(x)
+        want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+        assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
+        assert np.array_equal(lb, wl)
+    for shard in (0, 1):
+        sched = plan.e2e_schedule(75, shard)
+        assert sched is not None and sum(sched["chunks"]) == 75
