@@ -1,5 +1,6 @@
 """Turn an `ncu --metrics gpu__time_duration.sum --csv` launch list into a markdown table of
-one bench step (the launches between the first input pass and the following argmax)."""
+one bench step (from the first input pass / first conv to the following argmax, or to the
+next step when the last layer writes the labels itself)."""
 import csv
 import sys
 
@@ -14,7 +15,10 @@ def main(path, out, title):
     if not starts:  # the first conv checks its input itself (fused input pass): it opens the step
         starts = [i for i, k in enumerate(ks) if "first_conv" in k[1]]
     s0 = starts[0]
-    e0 = next(i for i in range(s0, len(ks)) if "argmax" in ks[i][1])
+    # ... to the step's argmax, or (labels fused into the last layer) up to the next step's start
+    e0 = next((i for i in range(s0, len(ks)) if "argmax" in ks[i][1]), None)
+    if e0 is None:
+        e0 = next((i - 1 for i in range(s0 + 1, len(ks)) if ks[i][1] == ks[s0][1]), len(ks) - 1)
     step = ks[s0:e0 + 1]
     tot = sum(k[2] for k in step) / 1e3
     with open(out, "w") as f:

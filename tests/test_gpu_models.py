@@ -316,3 +316,31 @@ def test_e2e_pipeline_two_shards():
     for shard in (0, 1):
         sched = plan.e2e_schedule(75, shard)
         assert sched is not None and sum(sched["chunks"]) == 75
+
+
+@pytest.mark.parametrize("hot", [(), (200, 260), (70, 63)])
+def test_fused_cross_tile_argmax_ties(hot):
+    """First-index argmax over many column tiles of the last FC (300 classes = 5 tiles of the
+    packed BMM): identical logits everywhere -> 0; a tie between two tiles -> the earlier
+    index; a tie across a tile boundary -> the earlier one (inference.hpp:177-184)."""
+    m = M.make_model("tie", "128FC", 16, 16, 1, 300, [])
+    fw = Wt.random_weights(m, 9)
+    last = fw.layers[-1]
+    U, K = m.layers[-1].units, m.layers[-1].in_channels
+    w = last["weights"].reshape(U, K)
+    w[:] = w[0]
+    for k in ("gamma", "mean", "var"):
+        last[k][:] = last[k][0]
+    last["gamma"][:] = abs(last["gamma"][0]) + 0.5
+    last["beta"][:] = 0.0
+    for h in hot:
+        last["beta"][h] = 100.0
+    ws = Wt.build_weights(m, fw)
+    x = np.random.default_rng(3).standard_normal((200, 16, 16, 1), dtype=np.float32)
+    plan = B.Plan(m, ws, 200)
+    for _ in range(2):  # (first run captures the graph, second replays it)
+        lg, lb = plan.run(x)
+        want, wl = oracle_run_inference(m.c_spec(), ws.c_store(), x)
+        assert np.array_equal(lg.view(np.uint64), want.view(np.uint64))
+        assert np.array_equal(lb, wl)
+        assert (lb == (min(hot) if hot else 0)).all()
